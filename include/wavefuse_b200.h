@@ -1,0 +1,151 @@
+/*
+ * wavefuse-b200 — C ABI of the B200-native DWT pan-sharpening hot path.
+ *
+ * This is the drop-in boundary. The reference (`wavefuse` 0.1.0, pure
+ * Python + numpy) has no plugin registry; its boundary is the Python function
+ * signatures of the hot path. Each entry point below replaces one of them and
+ * cites it (paths relative to /root/reference/pkg/src/wavefuse/):
+ *
+ *   wf_fuse_dwt_*          fusion.py:128-150  fuse_dwt(pan, ms_band, kind)
+ *   wf_fuse_bands_*        fusion.py:153-183  fuse(pan, ms, DwtReplace(kind)),
+ *                          the per-band loop of fusion.py:182 fused into one
+ *                          launch that reads PAN once
+ *   wf_fuse_strip_*        (new) one row strip of fuse_dwt with explicit halo
+ *                          rows, for the multi-GPU strip driver; replaces the
+ *                          per-tile wrap of tiling.py:213-273 with exact halos
+ *   wf_fuse_host_*         fuse() with HOST buffers: H2D, fuse, D2H pipelined
+ *                          in row strips (what WorkerServer.handle_task,
+ *                          cluster.py:297-299, or a ctypes caller would bind)
+ *   wf_dwt2d_forward_*     wavelet.py:149-155  dwt2d_forward(plane, kind)
+ *   wf_dwt2d_inverse_*     wavelet.py:158-164  dwt2d_inverse(coeffs, kind)
+ *   wf_dwt_rows_forward_*  wavelet.py:131-139  dwt1d_forward (nrows = 1)
+ *   wf_dwt_rows_inverse_*  wavelet.py:142-146  dwt1d_inverse (nrows = 1)
+ *   wf_resample_bilinear_* fusion.py:50-81     resample_bilinear(plane, w, h)
+ *   wf_degrade_*           metrics.py:31-42    degrade(plane, factor)
+ *   wf_q_index_*           metrics.py:45-83    q_index(a, b)
+ *   wf_quality_scene_f32   metrics.py:94-199   qnr()/ergas() partials
+ *
+ * Conventions
+ *  - All array arguments of the device entry points are DEVICE pointers;
+ *    pitches are in ELEMENTS. Arrays of band pointers (`ms`, `out`) are host
+ *    arrays of device pointers.
+ *  - `kind`: WF_HAAR = 1, WF_DAUB4 = 2 (the wire codes of cluster.py:81-83).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Every call is
+ *    asynchronous on that stream and re-entrant: no global scratch, so
+ *    concurrent callers on different streams/threads are safe
+ *    (tiling.py:185-189 and cluster.py:352-370 call fuse_dwt concurrently).
+ *  - Return 0 on success, else a WF_ERR_* code; wf_last_error() returns the
+ *    calling thread's message. The codes map 1:1 onto the reference's
+ *    exception classes (errors.py:32-73) in the Python shim.
+ *  - Dtype rule (wavelet.py:69-70, fusion.py:46-47): f32 in -> f32 out, f64
+ *    in -> f64 out. The f32 fused kernels compute in f32 (max-abs <= 1e-4 vs
+ *    the float64 reference on 0..255 data); the f64 ones in f64; the
+ *    standalone transforms and resample compute in f64 with the reference's
+ *    exact operation order (bit-identical results).
+ */
+#ifndef WAVEFUSE_B200_H
+#define WAVEFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  WF_HAAR = 1,
+  WF_DAUB4 = 2
+};
+
+enum {
+  WF_OK = 0,
+  WF_ERR_VALUE = 1,              /* ValueError (bad ndim/kind/pointer/size)   */
+  WF_ERR_ODD_DIMENSION = 2,      /* errors.OddDimension                        */
+  WF_ERR_TOO_SMALL = 3,          /* errors.TooSmall                            */
+  WF_ERR_DIMENSION_MISMATCH = 4, /* errors.DimensionMismatch                   */
+  WF_ERR_CUDA = 5,               /* CUDA runtime failure (RuntimeError)        */
+  WF_ERR_BAND_COUNT = 6,         /* errors.BandCountMismatch                   */
+  WF_ERR_ODD_LENGTH = 7,         /* errors.OddLength                           */
+  WF_ERR_TOO_SHORT = 8,          /* errors.TooShort                            */
+  WF_ERR_NOT_DIVISIBLE = 9       /* errors.NotDivisible                        */
+};
+
+#define WF_MAX_BANDS_PER_LAUNCH 8
+
+const char* wf_version(void);
+const char* wf_last_error(void);
+/* Number of kernel launches this thread has issued through the library. */
+int64_t wf_launch_count(void);
+
+/* ---- fused hot path (device buffers) ---------------------------------- */
+int wf_fuse_dwt_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,
+                    int64_t ms_pitch, float* out, int64_t out_pitch, int h, int w,
+                    void* stream);
+int wf_fuse_dwt_f64(int kind, const double* pan, int64_t pan_pitch, const double* ms,
+                    int64_t ms_pitch, double* out, int64_t out_pitch, int h, int w,
+                    void* stream);
+
+int wf_fuse_bands_f32(int kind, const float* pan, int64_t pan_pitch,
+                      const float* const* ms, int64_t ms_pitch, float* const* out,
+                      int64_t out_pitch, int nbands, int h, int w, void* stream);
+int wf_fuse_bands_f64(int kind, const double* pan, int64_t pan_pitch,
+                      const double* const* ms, int64_t ms_pitch, double* const* out,
+                      int64_t out_pitch, int nbands, int h, int w, void* stream);
+
+/* One strip of `rows` PAN rows (even). D4 needs pan_top = the 2 PAN rows
+ * above the strip, pan_bot = the 2 rows below (global periodic wrap applied
+ * by the caller), ms_top[b] = the MS row above the strip of band b. Haar
+ * ignores the halo pointers (may be NULL). */
+int wf_fuse_strip_f32(int kind, const float* pan, int64_t pan_pitch, const float* pan_top,
+                      const float* pan_bot, int64_t halo_pitch, const float* const* ms,
+                      const float* const* ms_top, int64_t ms_pitch, float* const* out,
+                      int64_t out_pitch, int nbands, int rows, int w, void* stream);
+int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const double* pan_top,
+                      const double* pan_bot, int64_t halo_pitch, const double* const* ms,
+                      const double* const* ms_top, int64_t ms_pitch, double* const* out,
+                      int64_t out_pitch, int nbands, int rows, int w, void* stream);
+
+/* ---- fused hot path (HOST buffers, contiguous rows) --------------------- */
+typedef struct wf_ctx wf_ctx;
+/* strip_rows: PAN rows per pipeline stage (even; 0 = default 512). */
+wf_ctx* wf_ctx_create(int device, int strip_rows);
+void wf_ctx_destroy(wf_ctx* ctx);
+int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const* ms,
+                     float* const* out, int nbands, int h, int w);
+int wf_fuse_host_f64(wf_ctx* ctx, int kind, const double* pan, const double* const* ms,
+                     double* const* out, int nbands, int h, int w);
+
+/* ---- standalone transforms --------------------------------------------- */
+int wf_dwt2d_forward_f32(int kind, const float* in, int64_t in_pitch, float* out,
+                         int64_t out_pitch, int h, int w, void* stream);
+int wf_dwt2d_forward_f64(int kind, const double* in, int64_t in_pitch, double* out,
+                         int64_t out_pitch, int h, int w, void* stream);
+int wf_dwt2d_inverse_f32(int kind, const float* in, int64_t in_pitch, float* out,
+                         int64_t out_pitch, int h, int w, void* stream);
+int wf_dwt2d_inverse_f64(int kind, const double* in, int64_t in_pitch, double* out,
+                         int64_t out_pitch, int h, int w, void* stream);
+int wf_dwt_rows_forward_f32(int kind, const float* in, int64_t in_pitch, float* out,
+                            int64_t out_pitch, int nrows, int n, void* stream);
+int wf_dwt_rows_forward_f64(int kind, const double* in, int64_t in_pitch, double* out,
+                            int64_t out_pitch, int nrows, int n, void* stream);
+int wf_dwt_rows_inverse_f32(int kind, const float* in, int64_t in_pitch, float* out,
+                            int64_t out_pitch, int nrows, int n, void* stream);
+int wf_dwt_rows_inverse_f64(int kind, const double* in, int64_t in_pitch, double* out,
+                            int64_t out_pitch, int nrows, int n, void* stream);
+
+int wf_resample_bilinear_f32(const float* in, int64_t in_pitch, int in_h, int in_w,
+                             float* out, int64_t out_pitch, int out_h, int out_w,
+                             void* stream);
+int wf_resample_bilinear_f64(const double* in, int64_t in_pitch, int in_h, int in_w,
+                             double* out, int64_t out_pitch, int out_h, int out_w,
+                             void* stream);
+
+/* ---- synthetic scenes (counter hash; numpy twin in synth.py) ------------ */
+int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
+                       uint32_t plane, int row0, int col0, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WAVEFUSE_B200_H */

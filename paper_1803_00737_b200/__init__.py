@@ -1,0 +1,63 @@
+"""wavefuse-b200: B200-native (sm_100a) drop-in for the DWT pan-sharpening hot
+path of the reference `wavefuse` package (arXiv 1803.00737).
+
+Same public names and signatures as the reference's hot-path subset
+(/root/reference/pkg/src/wavefuse/__init__.py:18-51): transforms, DWT fusion,
+bilinear resampling and the quality metrics. Compute runs only in the in-tree
+sm_100a library `libwavefuse_b200.so` (C ABI: include/wavefuse_b200.h); there
+is no CPU fallback.
+"""
+
+from .errors import (
+    BandCountMismatch,
+    CudaError,
+    DimensionMismatch,
+    FusionError,
+    NotDivisible,
+    OddDimension,
+    OddLength,
+    TooFewBands,
+    TooShort,
+    TooSmall,
+    ZeroBandMean,
+)
+from .fusion import DwtReplace, FusionMethod, fuse, fuse_dwt, method_from_name, resample_bilinear
+from .wavelet import (
+    FilterBank,
+    WaveletKind,
+    d4_filters,
+    dwt1d_forward,
+    dwt1d_inverse,
+    dwt2d_forward,
+    dwt2d_inverse,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BandCountMismatch",
+    "CudaError",
+    "DimensionMismatch",
+    "DwtReplace",
+    "FilterBank",
+    "FusionError",
+    "FusionMethod",
+    "NotDivisible",
+    "OddDimension",
+    "OddLength",
+    "TooFewBands",
+    "TooShort",
+    "TooSmall",
+    "WaveletKind",
+    "ZeroBandMean",
+    "__version__",
+    "d4_filters",
+    "dwt1d_forward",
+    "dwt1d_inverse",
+    "dwt2d_forward",
+    "dwt2d_inverse",
+    "fuse",
+    "fuse_dwt",
+    "method_from_name",
+    "resample_bilinear",
+]

@@ -1,0 +1,400 @@
+// wavefuse-b200: extern "C" boundary (include/wavefuse_b200.h).
+//
+// Validation mirrors the reference's preconditions and their order
+// (fusion.py:137-147 then wavelet.py:121-128 inside dwt2d_forward) so the
+// Python shim can map return codes onto the same exception classes.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/wavefuse_b200.h"
+#include "wf_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return WF_OK;
+  return fail(WF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int min_len(int kind) { return kind == WF_HAAR ? 2 : 4; }  // wavelet.py:66
+
+int check_kind(int kind) {
+  if (kind != WF_HAAR && kind != WF_DAUB4)
+    return fail(WF_ERR_VALUE, "unknown wavelet kind %d", kind);
+  return WF_OK;
+}
+
+// wavelet.py:121-128 (_check_2d, after the ndim test the shim does)
+int check_2d(int kind, int h, int w) {
+  if (int e = check_kind(kind)) return e;
+  if (h < min_len(kind) || w < min_len(kind))
+    return fail(WF_ERR_TOO_SMALL, "%dx%d below minimum %d per side", w, h, min_len(kind));
+  if ((h & 1) || (w & 1)) return fail(WF_ERR_ODD_DIMENSION, "%dx%d has an odd dimension", w, h);
+  return WF_OK;
+}
+
+// wavelet.py:112-118 (_check_1d)
+int check_1d(int kind, int n) {
+  if (int e = check_kind(kind)) return e;
+  if (n < min_len(kind)) return fail(WF_ERR_TOO_SHORT, "length %d below minimum %d", n, min_len(kind));
+  if (n & 1) return fail(WF_ERR_ODD_LENGTH, "length %d is odd", n);
+  return WF_OK;
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename T>
+int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, const T* pan_bot,
+                int64_t halo_pitch, const T* const* ms, const T* const* ms_top, int64_t ms_pitch,
+                T* const* out, int64_t out_pitch, int nbands, int rows, int w, bool strip,
+                cudaStream_t s) {
+  if (int e = check_kind(kind)) return e;
+  if (nbands < 1) return fail(WF_ERR_BAND_COUNT, "need at least one band");
+  if (!pan || !ms || !out) return fail(WF_ERR_VALUE, "null pointer argument");
+  // fusion.py:140-141 (odd) precedes the band-shape test; dwt2d_forward's
+  // TooSmall comes last (wavelet.py:124-126 via fusion.py:148)
+  if ((rows & 1) || (w & 1))
+    return fail(WF_ERR_ODD_DIMENSION, "panchromatic plane %dx%d has an odd dimension", w, rows);
+  if (!strip && (rows < min_len(kind) || w < min_len(kind)))
+    return fail(WF_ERR_TOO_SMALL, "%dx%d below minimum %d per side", w, rows, min_len(kind));
+  if (strip && (rows < 2 || w < min_len(kind)))
+    return fail(WF_ERR_TOO_SMALL, "strip %dx%d too small", w, rows);
+  if (pan_pitch < w || out_pitch < w || ms_pitch < w / 2)
+    return fail(WF_ERR_VALUE, "pitch smaller than row length");
+  if (kind == WF_DAUB4 && strip && (!pan_top || !pan_bot || !ms_top))
+    return fail(WF_ERR_VALUE, "D4 strip needs halo pointers");
+
+  const int vw = 16 / (int)sizeof(T);  // elements per 16 B
+  bool vec = al16(pan) && pan_pitch % vw == 0 && out_pitch % vw == 0 && ms_pitch % 2 == 0;
+  if (kind == WF_HAAR) vec = vec && (w % 4 == 0);
+  for (int b = 0; b < nbands; ++b) {
+    if (!ms[b] || !out[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
+    vec = vec && al16(out[b]) && al16(ms[b]);
+  }
+
+  wf::LaunchTuning tune{0, 0};
+  if (const char* e = getenv("WF_D4_TARGET_WARPS")) tune.d4_target_warps = atoi(e);
+  if (const char* e = getenv("WF_D4_MIN_PAIRS")) tune.d4_min_pairs = atoi(e);
+
+  for (int b0 = 0; b0 < nbands; b0 += wf::kMaxBandsPerLaunch) {
+    const int nb = nbands - b0 < wf::kMaxBandsPerLaunch ? nbands - b0 : wf::kMaxBandsPerLaunch;
+    wf::FuseArgs<T> a;
+    memset(&a, 0, sizeof a);
+    a.pan = pan;
+    a.pan_pitch = pan_pitch;
+    a.ms_pitch = ms_pitch;
+    a.out_pitch = out_pitch;
+    a.nbands = nb;
+    a.rows = rows;
+    a.W = w;
+    if (kind == WF_DAUB4) {
+      if (strip) {
+        a.pan_top = pan_top;
+        a.pan_bot = pan_bot;
+        a.halo_pitch = halo_pitch;
+        vec = vec && al16(pan_top) && al16(pan_bot) && halo_pitch % vw == 0;
+      } else {  // periodic wrap of the whole image (wavelet.py:83-84)
+        a.pan_top = pan + (int64_t)(rows - 2) * pan_pitch;
+        a.pan_bot = pan;
+        a.halo_pitch = pan_pitch;
+      }
+    }
+    for (int b = 0; b < nb; ++b) {
+      a.ms[b] = ms[b0 + b];
+      a.out[b] = out[b0 + b];
+      if (kind == WF_DAUB4)
+        a.ms_top[b] = strip ? ms_top[b0 + b]
+                            : ms[b0 + b] + (int64_t)(rows / 2 - 1) * ms_pitch;
+    }
+    cudaError_t e = wf::launch_fuse<T, T>(kind, a, vec, s, tune);
+    if (e != cudaSuccess) return cuda_status(e, "fuse launch");
+    ++g_launches;
+  }
+  return WF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline: rows are cut into strips; each strip's PAN rows, its
+// D4 halo rows and its MS rows go up, the strip kernel runs, the fused rows
+// come back. Three slots rotate over three streams so H2D of strip k+1, the
+// kernel of strip k and D2H of strip k-1 overlap (copy engines are
+// full-duplex on PCIe).
+// ---------------------------------------------------------------------------
+constexpr int kSlots = 3;
+
+struct Slot {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  void* dbuf = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct wf_ctx {
+  int device = 0;
+  int strip_rows = 512;
+  Slot slot[kSlots];
+};
+
+namespace {
+
+template <typename T>
+int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const* out,
+              int nbands, int h, int w) {
+  if (!ctx) return fail(WF_ERR_VALUE, "null context");
+  if (int e = check_kind(kind)) return e;
+  if (nbands < 1) return fail(WF_ERR_BAND_COUNT, "need at least one band");
+  if ((h & 1) || (w & 1))
+    return fail(WF_ERR_ODD_DIMENSION, "panchromatic plane %dx%d has an odd dimension", w, h);
+  if (h < min_len(kind) || w < min_len(kind))
+    return fail(WF_ERR_TOO_SMALL, "%dx%d below minimum %d per side", w, h, min_len(kind));
+  if (cudaError_t e = cudaSetDevice(ctx->device)) return cuda_status(e, "cudaSetDevice");
+
+  int S = ctx->strip_rows;
+  if (S > h) S = h;
+  const int wh = w / 2;
+  // device slot layout: pan [S][w] | pan_top[2][w] | pan_bot[2][w] |
+  //                     ms [B][S/2][wh] | ms_top [B][wh] | out [B][S][w]
+  const size_t pan_e = (size_t)S * w, halo_e = 2 * (size_t)w;
+  const size_t ms_e = (size_t)(S / 2) * wh, mst_e = (size_t)wh, out_e = (size_t)S * w;
+  auto up16 = [](size_t n) { return (n * sizeof(T) + 255) / 256 * 256 / sizeof(T); };
+  const size_t need_e = up16(pan_e) + 2 * up16(halo_e) +
+                        (size_t)nbands * (up16(ms_e) + up16(mst_e) + up16(out_e));
+  const size_t need = need_e * sizeof(T);
+  for (int k = 0; k < kSlots; ++k) {
+    Slot& sl = ctx->slot[k];
+    if (sl.bytes < need) {
+      if (sl.dbuf) cudaFree(sl.dbuf);
+      sl.dbuf = nullptr;
+      sl.bytes = 0;
+      if (cudaError_t e = cudaMalloc(&sl.dbuf, need)) return cuda_status(e, "cudaMalloc slot");
+      sl.bytes = need;
+    }
+  }
+
+  std::vector<const T*> dms(nbands), dmst(nbands);
+  std::vector<T*> dout(nbands);
+  int k = 0;
+  for (int r0 = 0; r0 < h; r0 += S, k = (k + 1) % kSlots) {
+    const int rows = (h - r0) < S ? (h - r0) : S;
+    Slot& sl = ctx->slot[k];
+    cudaStream_t st = sl.stream;
+    T* base = static_cast<T*>(sl.dbuf);
+    T* dpan = base;
+    T* dtop = dpan + up16(pan_e);
+    T* dbot = dtop + up16(halo_e);
+    T* cur = dbot + up16(halo_e);
+    for (int b = 0; b < nbands; ++b) {
+      T* dm = cur;
+      T* dmt = dm + up16(ms_e);
+      T* dot = dmt + up16(mst_e);
+      cur = dot + up16(out_e);
+      dms[b] = dm;
+      dmst[b] = dmt;
+      dout[b] = dot;
+    }
+    // the slot's previous strip must have finished its D2H before reuse
+    // (same stream => already ordered)
+    cudaError_t e = cudaMemcpyAsync(dpan, pan + (size_t)r0 * w, sizeof(T) * (size_t)rows * w,
+                                    cudaMemcpyHostToDevice, st);
+    if (kind == WF_DAUB4) {
+      for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+        const int rt = (r0 - 2 + q + h) % h, rb = (r0 + rows + q) % h;
+        e = cudaMemcpyAsync(dtop + (size_t)q * w, pan + (size_t)rt * w, sizeof(T) * w,
+                            cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(dbot + (size_t)q * w, pan + (size_t)rb * w, sizeof(T) * w,
+                              cudaMemcpyHostToDevice, st);
+      }
+    }
+    for (int b = 0; b < nbands && e == cudaSuccess; ++b) {
+      e = cudaMemcpyAsync(const_cast<T*>(dms[b]), ms[b] + (size_t)(r0 / 2) * wh,
+                          sizeof(T) * (size_t)(rows / 2) * wh, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess && kind == WF_DAUB4) {
+        const int mt = (r0 / 2 - 1 + h / 2) % (h / 2);
+        e = cudaMemcpyAsync(const_cast<T*>(dmst[b]), ms[b] + (size_t)mt * wh, sizeof(T) * wh,
+                            cudaMemcpyHostToDevice, st);
+      }
+    }
+    if (e != cudaSuccess) return cuda_status(e, "H2D");
+    if (int rc = fuse_common<T>(kind, dpan, w, dtop, dbot, w, dms.data(), dmst.data(), wh,
+                                dout.data(), w, nbands, rows, w, true, st))
+      return rc;
+    for (int b = 0; b < nbands && e == cudaSuccess; ++b)
+      e = cudaMemcpyAsync(out[b] + (size_t)r0 * w, dout[b], sizeof(T) * (size_t)rows * w,
+                          cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_status(e, "D2H");
+  }
+  for (int q = 0; q < kSlots; ++q)
+    if (cudaError_t e = cudaStreamSynchronize(ctx->slot[q].stream))
+      return cuda_status(e, "stream sync");
+  return WF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wf_version(void) { return "wavefuse-b200 0.1.0 (sm_100a)"; }
+const char* wf_last_error(void) { return g_err.c_str(); }
+int64_t wf_launch_count(void) { return g_launches; }
+
+int wf_fuse_dwt_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,
+                    int64_t ms_pitch, float* out, int64_t out_pitch, int h, int w,
+                    void* stream) {
+  return fuse_common<float>(kind, pan, pan_pitch, nullptr, nullptr, 0, &ms, nullptr, ms_pitch,
+                            &out, out_pitch, 1, h, w, false, (cudaStream_t)stream);
+}
+int wf_fuse_dwt_f64(int kind, const double* pan, int64_t pan_pitch, const double* ms,
+                    int64_t ms_pitch, double* out, int64_t out_pitch, int h, int w,
+                    void* stream) {
+  return fuse_common<double>(kind, pan, pan_pitch, nullptr, nullptr, 0, &ms, nullptr, ms_pitch,
+                             &out, out_pitch, 1, h, w, false, (cudaStream_t)stream);
+}
+int wf_fuse_bands_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
+                      int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
+                      int w, void* stream) {
+  return fuse_common<float>(kind, pan, pan_pitch, nullptr, nullptr, 0, ms, nullptr, ms_pitch,
+                            out, out_pitch, nbands, h, w, false, (cudaStream_t)stream);
+}
+int wf_fuse_bands_f64(int kind, const double* pan, int64_t pan_pitch, const double* const* ms,
+                      int64_t ms_pitch, double* const* out, int64_t out_pitch, int nbands, int h,
+                      int w, void* stream) {
+  return fuse_common<double>(kind, pan, pan_pitch, nullptr, nullptr, 0, ms, nullptr, ms_pitch,
+                             out, out_pitch, nbands, h, w, false, (cudaStream_t)stream);
+}
+int wf_fuse_strip_f32(int kind, const float* pan, int64_t pan_pitch, const float* pan_top,
+                      const float* pan_bot, int64_t halo_pitch, const float* const* ms,
+                      const float* const* ms_top, int64_t ms_pitch, float* const* out,
+                      int64_t out_pitch, int nbands, int rows, int w, void* stream) {
+  return fuse_common<float>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
+                            ms_pitch, out, out_pitch, nbands, rows, w, true,
+                            (cudaStream_t)stream);
+}
+int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const double* pan_top,
+                      const double* pan_bot, int64_t halo_pitch, const double* const* ms,
+                      const double* const* ms_top, int64_t ms_pitch, double* const* out,
+                      int64_t out_pitch, int nbands, int rows, int w, void* stream) {
+  return fuse_common<double>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
+                             ms_pitch, out, out_pitch, nbands, rows, w, true,
+                             (cudaStream_t)stream);
+}
+
+wf_ctx* wf_ctx_create(int device, int strip_rows) {
+  if (cudaError_t e = cudaSetDevice(device)) {
+    cuda_status(e, "cudaSetDevice");
+    return nullptr;
+  }
+  wf_ctx* c = new wf_ctx;
+  c->device = device;
+  if (strip_rows > 0) c->strip_rows = strip_rows & ~1;
+  if (c->strip_rows < 2) c->strip_rows = 2;
+  for (int k = 0; k < kSlots; ++k) {
+    if (cudaError_t e = cudaStreamCreateWithFlags(&c->slot[k].stream, cudaStreamNonBlocking)) {
+      cuda_status(e, "cudaStreamCreate");
+      wf_ctx_destroy(c);
+      return nullptr;
+    }
+  }
+  return c;
+}
+
+void wf_ctx_destroy(wf_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (int k = 0; k < kSlots; ++k) {
+    if (c->slot[k].stream) {
+      cudaStreamSynchronize(c->slot[k].stream);
+      cudaStreamDestroy(c->slot[k].stream);
+    }
+    if (c->slot[k].dbuf) cudaFree(c->slot[k].dbuf);
+  }
+  delete c;
+}
+
+int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const* ms,
+                     float* const* out, int nbands, int h, int w) {
+  return fuse_host<float>(ctx, kind, pan, ms, out, nbands, h, w);
+}
+int wf_fuse_host_f64(wf_ctx* ctx, int kind, const double* pan, const double* const* ms,
+                     double* const* out, int nbands, int h, int w) {
+  return fuse_host<double>(ctx, kind, pan, ms, out, nbands, h, w);
+}
+
+#define WF_DWT2D(NAME, T, INV)                                                               \
+  int NAME(int kind, const T* in, int64_t in_pitch, T* out, int64_t out_pitch, int h, int w, \
+           void* stream) {                                                                   \
+    if (int e = check_2d(kind, h, w)) return e;                                              \
+    if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");                     \
+    cudaError_t e = wf::launch_dwt2d<T>(kind, INV, in, in_pitch, out, out_pitch, h, w,       \
+                                        (cudaStream_t)stream);                               \
+    if (e == cudaSuccess) ++g_launches;                                                      \
+    return cuda_status(e, #NAME);                                                            \
+  }
+WF_DWT2D(wf_dwt2d_forward_f32, float, false)
+WF_DWT2D(wf_dwt2d_forward_f64, double, false)
+WF_DWT2D(wf_dwt2d_inverse_f32, float, true)
+WF_DWT2D(wf_dwt2d_inverse_f64, double, true)
+
+#define WF_ROWS(NAME, T, INV)                                                              \
+  int NAME(int kind, const T* in, int64_t in_pitch, T* out, int64_t out_pitch, int nrows, \
+           int n, void* stream) {                                                          \
+    if (int e = check_1d(kind, n)) return e;                                               \
+    if (nrows < 1) return fail(WF_ERR_VALUE, "nrows must be positive");                    \
+    if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");                   \
+    cudaError_t e = wf::launch_dwt_rows<T>(kind, INV, in, in_pitch, out, out_pitch, nrows, \
+                                           n, (cudaStream_t)stream);                       \
+    if (e == cudaSuccess) ++g_launches;                                                    \
+    return cuda_status(e, #NAME);                                                          \
+  }
+WF_ROWS(wf_dwt_rows_forward_f32, float, false)
+WF_ROWS(wf_dwt_rows_forward_f64, double, false)
+WF_ROWS(wf_dwt_rows_inverse_f32, float, true)
+WF_ROWS(wf_dwt_rows_inverse_f64, double, true)
+
+#define WF_RESAMPLE(NAME, T)                                                                 \
+  int NAME(const T* in, int64_t in_pitch, int in_h, int in_w, T* out, int64_t out_pitch,    \
+           int out_h, int out_w, void* stream) {                                            \
+    if (out_w < 1 || out_h < 1)                                                             \
+      return fail(WF_ERR_VALUE, "output size %dx%d must be positive", out_w, out_h);        \
+    if (in_w < 1 || in_h < 1) return fail(WF_ERR_VALUE, "empty input plane");              \
+    if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");                    \
+    cudaError_t e = wf::launch_resample<T>(in, in_pitch, in_h, in_w, out, out_pitch, out_h, \
+                                           out_w, (cudaStream_t)stream);                    \
+    if (e == cudaSuccess) ++g_launches;                                                     \
+    return cuda_status(e, #NAME);                                                           \
+  }
+WF_RESAMPLE(wf_resample_bilinear_f32, float)
+WF_RESAMPLE(wf_resample_bilinear_f64, double)
+
+int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
+                       uint32_t plane, int row0, int col0, void* stream) {
+  if (!out || rows < 0 || cols < 0 || pitch < cols)
+    return fail(WF_ERR_VALUE, "bad synth arguments");
+  if (rows == 0 || cols == 0) return WF_OK;
+  cudaError_t e = wf::launch_synth(out, pitch, rows, cols, seed, plane, row0, col0,
+                                   (cudaStream_t)stream);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e, "wf_synth_plane_f32");
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// wavefuse-b200: internal launcher interface between the C-ABI layer
+// (capi.cu) and the kernel translation units. Not part of the public ABI
+// (that is include/wavefuse_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wf {
+
+constexpr int kMaxBandsPerLaunch = 8;
+
+// Argument block of one fused launch over a (strip of a) scene. Passed by
+// value as the kernel parameter (well under the 4 KB limit).
+template <typename T>
+struct FuseArgs {
+  const T* pan;
+  long long pan_pitch;  // elements
+  // D4 halo row sources (2 rows each, pitch halo_pitch). For a whole image
+  // they alias rows H-2..H-1 and 0..1 of the image itself (periodic wrap).
+  const T* pan_top;
+  const T* pan_bot;
+  long long halo_pitch;
+  const T* ms[kMaxBandsPerLaunch];
+  const T* ms_top[kMaxBandsPerLaunch];  // D4: MS row i0-1 of each band
+  long long ms_pitch;
+  T* out[kMaxBandsPerLaunch];
+  long long out_pitch;
+  int nbands;
+  int rows;  // PAN rows in this launch (even)
+  int W;     // PAN columns (even)
+  // filled by the launcher
+  int pairs_per_task;
+  int n_colbands;
+  long long n_tasks;
+};
+
+struct LaunchTuning {
+  int d4_target_warps;  // <=0: occupancy x SMs
+  int d4_min_pairs;     // <=0: no minimum
+};
+
+template <typename T, typename Acc>
+cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, cudaStream_t s,
+                        const LaunchTuning& tune);
+
+// Standalone transforms (materialise coefficients; wavelet.py:131-164).
+template <typename T>
+cudaError_t launch_dwt2d(int kind, bool inverse, const T* in, long long in_pitch, T* out,
+                         long long out_pitch, int h, int w, cudaStream_t s);
+template <typename T>
+cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long in_pitch, T* out,
+                            long long out_pitch, int nrows, int n, cudaStream_t s);
+
+// fusion.py:50-81
+template <typename T>
+cudaError_t launch_resample(const T* in, long long in_pitch, int in_h, int in_w, T* out,
+                            long long out_pitch, int out_h, int out_w, cudaStream_t s);
+
+// Counter-hash synthetic plane (uniform [0,255) f32), numpy twin in
+// paper_1803_00737_b200/synth.py.
+cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsigned long long seed,
+                         unsigned plane, int row0, int col0, cudaStream_t s);
+
+}  // namespace wf

@@ -1,0 +1,197 @@
+"""DWT coefficient-replacement fusion, GPU-backed.
+
+Drop-in for the hot path of /root/reference/pkg/src/wavefuse/fusion.py:
+`fuse_dwt` (fusion.py:128-150), the `fuse` dispatcher for `DwtReplace`
+(fusion.py:153-183), `resample_bilinear` (fusion.py:50-81) and
+`method_from_name` (fusion.py:186-196). Same signatures, same validation
+order and exception classes (raised before any compute), same dtype rule.
+
+Compute: `fuse` sends all bands of a scene through ONE launch of the fused
+kernel (csrc/fuse.cu) that reads PAN once and never materialises the
+coefficient image; `fuse_dwt` is the one-band case of the same kernel, so
+`fuse(...)[k]` equals `fuse_dwt(pan, ms[k], kind)` bit for bit (the
+reference's test_fusion.py:168-187 contract).
+
+numpy inputs go through the library's host-buffer pipeline
+(wf_fuse_host_*: H2D, fuse and D2H overlapped in row strips); CUDA tensors
+stay on the device (wf_fuse_bands_*).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .errors import BandCountMismatch, DimensionMismatch, OddDimension, TooSmall
+from .wavelet import KIND_CODE, MIN_LEN, WaveletKind
+
+
+@dataclass(frozen=True)
+class DwtReplace:
+    """fusion.py:35-40: swap the approximation quadrant of the PAN transform
+    for the band data, then invert."""
+
+    kind: WaveletKind
+
+
+FusionMethod = DwtReplace
+
+# fusion.py:125: Haar (averaging form) has unit DC gain, orthonormal D4 gain 2.
+LL_GAIN = {WaveletKind.HAAR: 1.0, WaveletKind.DAUB4: 2.0}
+
+
+def _shape(x):
+    return tuple(x.shape) if isinstance(x, torch.Tensor) else np.shape(x)
+
+
+def _is_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+# ---------------------------------------------------------------------------
+# resample_bilinear (fusion.py:50-81)
+# ---------------------------------------------------------------------------
+def resample_bilinear(plane, out_w: int, out_h: int):
+    """Pixel-centre bilinear resampling, clamped to the source extent.
+    Unchanged dimensions return a fresh copy (fusion.py:64-65)."""
+    if not _is_tensor(plane):
+        plane = np.asarray(plane)
+    shape = _shape(plane)
+    if len(shape) != 2:
+        raise ValueError(f"expected a 2D array, got shape {shape}")
+    if out_w < 1 or out_h < 1:
+        raise ValueError(f"output size {out_w}x{out_h} must be positive")
+    in_h, in_w = shape
+    dt = _device.np_out_dtype(plane)
+    if (out_w, out_h) == (in_w, in_h):
+        if _is_tensor(plane):
+            return plane.to(_device.torch_dtype(dt)).clone()
+        return plane.astype(dt)
+    d_in = _device.to_device(plane, dt)
+    d_out = torch.empty((out_h, out_w), dtype=d_in.dtype, device=d_in.device)
+    lib = _native.load()
+    fn = lib.wf_resample_bilinear_f32 if dt == np.float32 else lib.wf_resample_bilinear_f64
+    _native.check(fn(d_in.data_ptr(), in_w, in_h, in_w, d_out.data_ptr(), out_w, out_h, out_w,
+                     _device.stream_ptr()))
+    return d_out if _is_tensor(plane) else d_out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# fused path
+# ---------------------------------------------------------------------------
+def _validate_pair(pan_shape, band_shape) -> tuple[int, int]:
+    """fusion.py:137-147, then dwt2d_forward's _check_2d (wavelet.py:121-128)."""
+    if len(pan_shape) != 2 or len(band_shape) != 2:
+        raise ValueError("expected 2D arrays")
+    h, w = pan_shape
+    if h % 2 or w % 2:
+        raise OddDimension(f"panchromatic plane {w}x{h} has an odd dimension")
+    if tuple(band_shape) != (h // 2, w // 2):
+        raise DimensionMismatch(
+            f"band is {band_shape[1]}x{band_shape[0]}, need {w // 2}x{h // 2}"
+        )
+    return h, w
+
+
+def _check_min(h: int, w: int, kind: WaveletKind) -> None:
+    if h < MIN_LEN[kind] or w < MIN_LEN[kind]:
+        raise TooSmall(f"{w}x{h} below minimum {MIN_LEN[kind]} per side")
+
+
+def _fuse_device(pan_t: torch.Tensor, bands_t: list[torch.Tensor], kind: WaveletKind,
+                 out_dt) -> list[torch.Tensor]:
+    """All bands in one library call on device-resident tensors."""
+    h, w = pan_t.shape
+    outs = [torch.empty((h, w), dtype=pan_t.dtype, device=pan_t.device) for _ in bands_t]
+    lib = _native.load()
+    fn = lib.wf_fuse_bands_f32 if out_dt == np.float32 else lib.wf_fuse_bands_f64
+    ms_ptrs = _native.ptr_array([b.data_ptr() for b in bands_t])
+    out_ptrs = _native.ptr_array([o.data_ptr() for o in outs])
+    _native.check(fn(KIND_CODE[kind], pan_t.data_ptr(), w, ms_ptrs, w // 2, out_ptrs, w,
+                     len(bands_t), h, w, _device.stream_ptr()))
+    return outs
+
+
+def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
+               out_dt) -> list[np.ndarray]:
+    """All bands through the library's host-buffer pipeline (H2D / fuse / D2H
+    overlapped per row strip)."""
+    h, w = pan.shape
+    pan_c = np.ascontiguousarray(pan, dtype=out_dt)
+    band_c = [np.ascontiguousarray(b, dtype=out_dt) for b in bands]
+    outs = [np.empty((h, w), dtype=out_dt) for _ in bands]
+    lib = _native.load()
+    ctx = _device.host_ctx()
+    fn = lib.wf_fuse_host_f32 if out_dt == np.float32 else lib.wf_fuse_host_f64
+    ms_ptrs = _native.ptr_array([b.ctypes.data for b in band_c])
+    out_ptrs = _native.ptr_array([o.ctypes.data for o in outs])
+    torch.cuda.current_stream().synchronize()
+    _native.check(fn(ctx, KIND_CODE[kind], pan_c.ctypes.data, ms_ptrs, out_ptrs, len(bands),
+                     h, w))
+    return outs
+
+
+def fuse_dwt(pan, ms_band, kind: WaveletKind):
+    """fusion.py:128-150: transform PAN, overwrite LL with band * gain,
+    invert. The band must be exactly half the PAN size per axis. Output dtype
+    follows the PAN (float32 iff PAN is float32)."""
+    if not _is_tensor(pan):
+        pan = np.asarray(pan)
+    if not _is_tensor(ms_band):
+        ms_band = np.asarray(ms_band)
+    h, w = _validate_pair(_shape(pan), _shape(ms_band))
+    _check_min(h, w, kind)
+    out_dt = _device.np_out_dtype(pan)
+    if _is_tensor(pan):
+        pan_t = _device.to_device(pan, out_dt)
+        return _fuse_device(pan_t, [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
+    return _fuse_host(pan, [np.asarray(ms_band)], kind, out_dt)[0]
+
+
+def fuse(pan, ms, method: FusionMethod):
+    """fusion.py:153-183 for DwtReplace: validate the band list, resample
+    bands that are not already half-size (bilinear, on the GPU), then fuse
+    every band. One launch reads PAN once for up to 8 bands."""
+    if not _is_tensor(pan):
+        pan = np.asarray(pan)
+    bands = [b if _is_tensor(b) else np.asarray(b) for b in ms]
+    if not bands:
+        raise BandCountMismatch("need at least one band")
+    first = _shape(bands[0])
+    for b in bands[1:]:
+        if _shape(b) != first:
+            raise DimensionMismatch(f"band sizes differ: {_shape(b)} vs {first}")
+    if not isinstance(method, DwtReplace):
+        # WA / IHS are outside the north-star path
+        raise TypeError(f"unknown fusion method {method!r}")
+    shape = _shape(pan)
+    if len(shape) != 2:
+        raise ValueError("expected 2D arrays")
+    h, w = shape
+    if h % 2 or w % 2:
+        raise OddDimension(f"panchromatic plane {w}x{h} has an odd dimension")
+    half = (h // 2, w // 2)
+    resampled = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0])
+                 for b in bands]
+    for b in resampled:
+        _validate_pair(shape, _shape(b))
+    _check_min(h, w, method.kind)
+    out_dt = _device.np_out_dtype(pan)
+    if _is_tensor(pan) or any(_is_tensor(b) for b in resampled):
+        pan_t = _device.to_device(pan, out_dt)
+        bands_t = [_device.to_device(b, out_dt) for b in resampled]
+        outs = _fuse_device(pan_t, bands_t, method.kind, out_dt)
+        return outs if _is_tensor(pan) else [o.cpu().numpy() for o in outs]
+    return _fuse_host(pan, resampled, method.kind, out_dt)
+
+
+def method_from_name(name: str, weight: float = 0.5) -> FusionMethod:
+    """fusion.py:186-196 (the DWT names; wa/ihs are out of scope here)."""
+    if name == "hdwt":
+        return DwtReplace(WaveletKind.HAAR)
+    if name == "ddwt":
+        return DwtReplace(WaveletKind.DAUB4)
+    raise ValueError(f"unknown method name {name!r}")

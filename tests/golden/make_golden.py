@@ -1,0 +1,153 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the reference package `wavefuse` (pure Python + numpy, read-only at
+/root/reference/pkg/src) and records its outputs on seeded inputs into
+tests/golden/*.npz. The reference does not travel to the GPU box, so these
+committed fixtures are how the GPU tests (and the oracle pinning tests) see
+the reference's exact answers. Re-running this script must reproduce the
+files bit for bit (the inputs are seeded).
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from wavefuse import fusion, metrics, wavelet  # noqa: E402  (the reference)
+
+OUT = Path(__file__).resolve().parent
+HAAR, D4 = wavelet.WaveletKind.HAAR, wavelet.WaveletKind.DAUB4
+
+# (name, h, w, bands, dtype): covers tiny wrap-aliasing shapes (4x4), widths
+# with W % 4 == 2, widths spanning several 128-column warp bands with and
+# without the vectorised interior, and a float64 case.
+FUSION_CASES = [
+    ("f4x4", 4, 4, 1, np.float32),
+    ("f6x10", 6, 10, 2, np.float32),
+    ("f8x12", 8, 12, 1, np.float32),
+    ("f16x16", 16, 16, 3, np.float32),
+    ("f34x70", 34, 70, 2, np.float32),
+    ("f24x392", 24, 392, 3, np.float32),
+    ("f40x262", 40, 262, 2, np.float32),
+    ("f10x520", 10, 520, 6, np.float32),
+    ("d36x264", 36, 264, 2, np.float64),
+    ("d10x6", 10, 6, 1, np.float64),
+]
+
+TRANSFORM_SHAPES = [(4, 4), (6, 10), (8, 12), (34, 70), (64, 64), (2, 2), (2, 6)]
+VECTOR_LENGTHS = [2, 4, 10, 64, 126]
+RESAMPLE_CASES = [((3, 5), (7, 11)), ((7, 8), (14, 16)), ((5, 5), (2, 3)), ((4, 4), (4, 8)),
+                  ((16, 24), (32, 48))]
+
+
+def fusion_golden():
+    rng = np.random.default_rng(20261018)
+    data = {}
+    for name, h, w, nb, dt in FUSION_CASES:
+        pan = rng.uniform(0.0, 255.0, (h, w)).astype(dt)
+        bands = [rng.uniform(0.0, 255.0, (h // 2, w // 2)).astype(dt) for _ in range(nb)]
+        data[f"{name}/pan"] = pan
+        for b, band in enumerate(bands):
+            data[f"{name}/ms{b}"] = band
+        for kind in (HAAR, D4):
+            if min(h, w) < 4 and kind is D4:
+                continue
+            outs = fusion.fuse(pan, bands, fusion.DwtReplace(kind))
+            for b, o in enumerate(outs):
+                data[f"{name}/{kind.value}/out{b}"] = o
+    # resampling dispatch: bands not at half size (fusion.py:177-181)
+    pan = rng.uniform(0.0, 255.0, (12, 16)).astype(np.float32)
+    odd = [rng.uniform(0.0, 255.0, (5, 7)).astype(np.float32) for _ in range(2)]
+    data["resamp/pan"] = pan
+    for b, band in enumerate(odd):
+        data[f"resamp/ms{b}"] = band
+    for kind in (HAAR, D4):
+        for b, o in enumerate(fusion.fuse(pan, odd, fusion.DwtReplace(kind))):
+            data[f"resamp/{kind.value}/out{b}"] = o
+    np.savez_compressed(OUT / "fusion.npz", **data)
+
+
+def transform_golden():
+    rng = np.random.default_rng(7)
+    data = {}
+    for h, w in TRANSFORM_SHAPES:
+        for dt in (np.float32, np.float64):
+            x = rng.uniform(0.0, 255.0, (h, w)).astype(dt)
+            c = rng.uniform(-255.0, 255.0, (h, w)).astype(dt)
+            tag = f"{h}x{w}/{np.dtype(dt).name}"
+            data[f"{tag}/x"] = x
+            data[f"{tag}/c"] = c
+            for kind in (HAAR, D4):
+                if min(h, w) < wavelet._MIN_LEN[kind]:
+                    continue
+                data[f"{tag}/{kind.value}/fwd"] = wavelet.dwt2d_forward(x, kind)
+                data[f"{tag}/{kind.value}/inv"] = wavelet.dwt2d_inverse(c, kind)
+    for n in VECTOR_LENGTHS:
+        for dt in (np.float32, np.float64):
+            x = rng.uniform(0.0, 255.0, n).astype(dt)
+            tag = f"v{n}/{np.dtype(dt).name}"
+            data[f"{tag}/x"] = x
+            for kind in (HAAR, D4):
+                if n < wavelet._MIN_LEN[kind]:
+                    continue
+                data[f"{tag}/{kind.value}/fwd"] = wavelet.dwt1d_forward(x, kind)
+                data[f"{tag}/{kind.value}/inv"] = wavelet.dwt1d_inverse(x, kind)
+    for k, ((ih, iw), (oh, ow)) in enumerate(RESAMPLE_CASES):
+        for dt in (np.float32, np.float64):
+            x = rng.uniform(0.0, 255.0, (ih, iw)).astype(dt)
+            tag = f"rs{k}/{np.dtype(dt).name}"
+            data[f"{tag}/x"] = x
+            data[f"{tag}/out"] = fusion.resample_bilinear(x, ow, oh)
+    np.savez_compressed(OUT / "transforms.npz", **data)
+
+
+def metrics_golden():
+    rng = np.random.default_rng(99)
+    data = {}
+    # q_index on shapes with partial edge blocks and sub-block planes
+    for k, (h, w) in enumerate([(33, 70), (40, 40), (16, 16), (64, 96), (31, 65)]):
+        a = rng.uniform(0.0, 255.0, (h, w))
+        b = a * 0.7 + rng.uniform(0.0, 60.0, (h, w))
+        data[f"q{k}/a"] = a
+        data[f"q{k}/b"] = b
+        data[f"q{k}/q"] = np.float64(metrics.q_index(a, b))
+    # degenerate blocks (den == 0): constant and zero-mean blocks
+    a = np.full((64, 64), 5.0)
+    b = a.copy()
+    b[32:, 32:] = 7.0
+    b[:32, 32:] = rng.uniform(0, 255, (32, 32))
+    data["qdeg/a"], data["qdeg/b"] = a, b
+    data["qdeg/q"] = np.float64(metrics.q_index(a, b))
+    # full reports on fused scenes
+    for k, (size, nb, kind) in enumerate([(64, 3, HAAR), (64, 3, D4), (96, 4, D4), (48, 2, HAAR)]):
+        pan = rng.uniform(0.0, 255.0, (size, size)).astype(np.float32)
+        ms = [rng.uniform(1.0, 255.0, (size // 2, size // 2)).astype(np.float32)
+              for _ in range(nb)]
+        fused = fusion.fuse(pan, ms, fusion.DwtReplace(kind))
+        rep = metrics.qnr(fused, ms, pan)
+        tag = f"rep{k}"
+        data[f"{tag}/pan"] = pan
+        for b in range(nb):
+            data[f"{tag}/ms{b}"] = ms[b]
+            data[f"{tag}/fused{b}"] = fused[b]
+        data[f"{tag}/ergas"] = np.float64(rep.ergas)
+        data[f"{tag}/q_per_band"] = np.array(rep.q_per_band)
+        data[f"{tag}/d_lambda"] = np.float64(rep.d_lambda)
+        data[f"{tag}/d_s"] = np.float64(rep.d_s)
+        data[f"{tag}/qnr"] = np.float64(rep.qnr)
+        data[f"{tag}/degrade0"] = metrics.degrade(fused[0], 2)
+    np.savez_compressed(OUT / "metrics.npz", **data)
+
+
+if __name__ == "__main__":
+    fusion_golden()
+    transform_golden()
+    metrics_golden()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)
