@@ -90,9 +90,14 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
     vec = vec && al16(out[b]) && al16(ms[b]);
   }
 
-  wf::LaunchTuning tune{0, 0};
+  wf::LaunchTuning tune{0, 0, 0, 0};
   if (const char* e = getenv("WF_D4_TARGET_WARPS")) tune.d4_target_warps = atoi(e);
   if (const char* e = getenv("WF_D4_MIN_PAIRS")) tune.d4_min_pairs = atoi(e);
+  if (const char* e = getenv("WF_D4_PAIRS")) tune.d4_pairs = atoi(e);
+  if (const char* e = getenv("WF_D4_STAGES")) tune.d4_stages = atoi(e);
+  const char* path = getenv("WF_D4_PATH");  // "ldg" forces the register-path kernel
+  const bool allow_tma = !(path && strcmp(path, "ldg") == 0);
+  auto row16 = [](int64_t pitch) { return (pitch * (int64_t)sizeof(T)) % 16 == 0; };
 
   for (int b0 = 0; b0 < nbands; b0 += wf::kMaxBandsPerLaunch) {
     const int nb = nbands - b0 < wf::kMaxBandsPerLaunch ? nbands - b0 : wf::kMaxBandsPerLaunch;
@@ -124,7 +129,10 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
         a.ms_top[b] = strip ? ms_top[b0 + b]
                             : ms[b0 + b] + (int64_t)(rows / 2 - 1) * ms_pitch;
     }
-    cudaError_t e = wf::launch_fuse<T, T>(kind, a, vec, s, tune);
+    bool tma = allow_tma && kind == WF_DAUB4 && vec && w % 8 == 0 && row16(pan_pitch) &&
+               row16(ms_pitch) && row16(a.halo_pitch) && al16(a.pan_top) && al16(a.pan_bot);
+    for (int b = 0; b < nb && tma; ++b) tma = al16(a.ms_top[b]);
+    cudaError_t e = wf::launch_fuse<T, T>(kind, a, vec, tma, s, tune);
     if (e != cudaSuccess) return cuda_status(e, "fuse launch");
     ++g_launches;
   }

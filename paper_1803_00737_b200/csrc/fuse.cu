@@ -189,14 +189,20 @@ __global__ void __launch_bounds__(kD4Threads)
 
   // ---- march -------------------------------------------------------------
   for (int i = i0; i < i1; ++i) {
+    // issue every load of the step before any arithmetic: 2 PAN rows + one
+    // MS row per band are in flight together
     Acc pn[2][4], rn[2][2], rln[2];
-    {
-      Acc xl[2] = {0, 0}, xr[2] = {0, 0};
-      L.load_pan(pan.row(2 * i + 2), pn[0], xl, xr);
-      L.rowpass(pn[0], xl, xr, h0, h1, h2, h3, rn[0], rln[0]);
-      L.load_pan(pan.row(2 * i + 3), pn[1], xl, xr);
-      L.rowpass(pn[1], xl, xr, h0, h1, h2, h3, rn[1], rln[1]);
+    Acc xl[2][2] = {{0, 0}, {0, 0}}, xr[2][2] = {{0, 0}, {0, 0}};
+    L.load_pan(pan.row(2 * i + 2), pn[0], xl[0], xr[0]);
+    L.load_pan(pan.row(2 * i + 3), pn[1], xl[1], xr[1]);
+    Acc ms_cur[NB][2], ms_lo[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      ms_lo[b] = 0;
+      L.load_ms(a.ms[b] + (long long)i * a.ms_pitch, ms_cur[b], ms_lo[b]);
     }
+    L.rowpass(pn[0], xl[0], xr[0], h0, h1, h2, h3, rn[0], rln[0]);
+    L.rowpass(pn[1], xl[1], xr[1], h0, h1, h2, h3, rn[1], rln[1]);
     Acc ll[3];
     ll[0] = dot4(h0, h1, h2, h3, ra[0][0], ra[1][0], rn[0][0], rn[1][0]);
     ll[1] = dot4(h0, h1, h2, h3, ra[0][1], ra[1][1], rn[0][1], rn[1][1]);
@@ -204,8 +210,8 @@ __global__ void __launch_bounds__(kD4Threads)
 
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      Acc m[2], mm = 0;
-      L.load_ms(a.ms[b] + (long long)i * a.ms_pitch, m, mm);
+      const Acc(&m)[2] = ms_cur[b];
+      const Acc mm = ms_lo[b];
       const Acc e0 = m[0] + m[0] - ll[0];
       const Acc e1 = m[1] + m[1] - ll[1];
       const Acc em = mm + mm - ll[2];
@@ -352,6 +358,7 @@ static cudaError_t launch_nb(int kind, const FuseArgs<T>& a0, bool vec, cudaStre
   a.pairs_per_task = (npairs + n_row - 1) / n_row;
   if (tune.d4_min_pairs > 0 && a.pairs_per_task < tune.d4_min_pairs)
     a.pairs_per_task = tune.d4_min_pairs < npairs ? tune.d4_min_pairs : npairs;
+  if (tune.d4_pairs > 0) a.pairs_per_task = tune.d4_pairs < npairs ? tune.d4_pairs : npairs;
   n_row = (npairs + a.pairs_per_task - 1) / a.pairs_per_task;
   a.n_tasks = (long long)n_row * a.n_colbands;
   const long long blocks = (a.n_tasks + (kD4Threads / 32) - 1) / (kD4Threads / 32);
@@ -363,8 +370,9 @@ static cudaError_t launch_nb(int kind, const FuseArgs<T>& a0, bool vec, cudaStre
 }
 
 template <typename T, typename Acc>
-cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, cudaStream_t s,
+cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, bool tma, cudaStream_t s,
                         const LaunchTuning& tune) {
+  if (kind == kDaub4 && tma) return launch_fuse_d4_tma<T>(a, s, tune);
   switch (a.nbands) {
     case 1: return launch_nb<T, Acc, 1>(kind, a, vec, s, tune);
     case 2: return launch_nb<T, Acc, 2>(kind, a, vec, s, tune);
@@ -378,9 +386,9 @@ cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, cudaStream_t s
   }
 }
 
-template cudaError_t launch_fuse<float, float>(int, const FuseArgs<float>&, bool, cudaStream_t,
-                                               const LaunchTuning&);
-template cudaError_t launch_fuse<double, double>(int, const FuseArgs<double>&, bool,
+template cudaError_t launch_fuse<float, float>(int, const FuseArgs<float>&, bool, bool,
+                                               cudaStream_t, const LaunchTuning&);
+template cudaError_t launch_fuse<double, double>(int, const FuseArgs<double>&, bool, bool,
                                                  cudaStream_t, const LaunchTuning&);
 
 }  // namespace wf

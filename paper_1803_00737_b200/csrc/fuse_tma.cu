@@ -1,0 +1,277 @@
+// wavefuse-b200: bulk-copy (TMA) pipelined D4 fusion kernel for sm_100a.
+//
+// Same maths as fuse_d4_kernel in fuse.cu (out = pan + S_LL(2 ms - LL(pan)),
+// SURVEY.md F2, reference fusion.py:128-150) and the same expression trees,
+// so the two kernels are bit-identical; this one moves the data differently:
+//
+//  * A CTA owns a column band of CW = 128*NCW PAN columns and a run of row
+//    pairs [i0, i1). Warp NCW is the producer: for every row pair it issues
+//    cp.async.bulk copies (UBLKCP) of the two new PAN rows -- each as a
+//    16-byte left halo piece, the main span, and a 16-byte right halo piece,
+//    with the periodic wrap applied to the halo pieces' source columns -- and
+//    of one MS row per band (left halo + span) into a ring of S shared-memory
+//    slots, signalling an mbarrier with the transaction bytes.
+//  * NCW consumer warps wait on the slot's full barrier, read their columns
+//    (plus the +-2 column halo) straight from shared memory -- no shuffles,
+//    no lane-0/lane-31 special cases -- release the slot (empty barrier) and
+//    stream the fused rows of every band to HBM with st.global.cs.
+//
+// Bytes in flight live in shared memory, not in registers, so a handful of
+// warps per SM keep >100 KB of HBM reads outstanding.
+#include "wf_common.cuh"
+#include "wf_kernels.h"
+#include "wf_tma.cuh"
+
+namespace wf {
+
+template <typename Acc>
+__device__ __forceinline__ Acc dot4t(Acc h0, Acc h1, Acc h2, Acc h3, Acc x0, Acc x1, Acc x2,
+                                     Acc x3) {
+  return fma(h3, x3, fma(h2, x2, fma(h1, x1, h0 * x0)));
+}
+
+template <typename T>
+struct TmaRows {
+  const T* main;
+  const T* top;
+  const T* bot;
+  long long pitch, halo_pitch;
+  int rows;
+  __device__ __forceinline__ const T* row(int r) const {
+    if (r < 0) return top + (long long)(r + 2) * halo_pitch;
+    if (r >= rows) return bot + (long long)(r - rows) * halo_pitch;
+    return main + (long long)r * pitch;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void lds2(const T* p, T& x, T& y) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    x = v.x;
+    y = v.y;
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    x = v.x;
+    y = v.y;
+  }
+}
+
+template <typename T, int NB, int NCW>
+__global__ void __launch_bounds__(32 * (NCW + 1))
+    fuse_d4_tma_kernel(const FuseArgs<T> a, int S) {
+  using Acc = T;
+  constexpr int CW = 128 * NCW;
+  constexpr int PROW = CW + 8;     // [4 left halo | CW | 4 right halo]
+  constexpr int MROW = CW / 2 + 4;  // [4 left halo | CW/2]
+  constexpr int SLOT = 2 * PROW + NB * MROW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* slots = reinterpret_cast<T*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * SLOT * sizeof(T));
+  uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb = (int)(blockIdx.x % (unsigned)a.n_colbands);
+  const int rt = (int)(blockIdx.x / (unsigned)a.n_colbands);
+  const int W = a.W, Wh = a.W >> 1;
+  const int base = cb * CW;
+  const int len = min(CW, W - base);
+  const int npairs = a.rows >> 1;
+  const int i0 = rt * a.pairs_per_task;
+  const int i1 = min(i0 + a.pairs_per_task, npairs);
+  const int nloads = (i1 - i0) + 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], NCW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------ producer ------------------------------
+    const TmaRows<T> pan{a.pan, a.pan_top, a.pan_bot, a.pan_pitch, a.halo_pitch, a.rows};
+    const uint32_t pan_row_bytes = (uint32_t)((len + 8) * sizeof(T));
+    const uint32_t ms_row_bytes = (uint32_t)((len / 2 + 4) * sizeof(T));
+    // per-lane copy role (fixed for the whole task)
+    const int q = lane / 3, piece = lane % 3;  // lanes 0..5: PAN row q, piece
+    const int mb = (lane - 6) >> 1, mpiece = (lane - 6) & 1;  // lanes 6..: MS band, piece
+    const int lcol = wrap(base - 4, W), rcol = (base + len) % W;
+    const int mlcol = wrap((base >> 1) - 4, Wh);
+    for (int n = 0; n < nloads; ++n) {
+      const int s = n % S, r = n / S;
+      if (r > 0 && lane == 0) tma::mbar_wait(&empty[s], (r - 1) & 1);
+      __syncwarp();
+      const bool with_ms = n >= 1;
+      if (lane == 0)
+        tma::mbar_arrive_expect_tx(&full[s],
+                                   2 * pan_row_bytes + (with_ms ? NB * ms_row_bytes : 0u));
+      __syncwarp();
+      T* slot = slots + (size_t)s * SLOT;
+      const int k = n - 2;  // row pair index relative to i0
+      if (lane < 6) {
+        const T* row = pan.row(2 * (i0 + k) + 2 + q);
+        T* dst = slot + q * PROW;
+        if (piece == 0)
+          tma::bulk_g2s(dst, row + lcol, 4 * sizeof(T), &full[s]);
+        else if (piece == 1)
+          tma::bulk_g2s(dst + 4, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
+        else
+          tma::bulk_g2s(dst + 4 + len, row + rcol, 4 * sizeof(T), &full[s]);
+      } else if (with_ms && lane < 6 + 2 * NB) {
+        const int mrow = i0 + k;
+        const T* mr = mrow < 0 ? a.ms_top[mb] : a.ms[mb] + (long long)mrow * a.ms_pitch;
+        T* dst = slot + 2 * PROW + mb * MROW;
+        if (mpiece == 0)
+          tma::bulk_g2s(dst, mr + mlcol, 4 * sizeof(T), &full[s]);
+        else
+          tma::bulk_g2s(dst + 4, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumers -------------------------------
+  const D4 tp = d4_taps();
+  const Acc h0 = (Acc)tp.h0, h1 = (Acc)tp.h1, h2 = (Acc)tp.h2, h3 = (Acc)tp.h3;
+  const int t = warp * 32 + lane;
+  const int rel = 4 * t;
+  const bool valid = rel < len;
+  const int c = base + rel;
+
+  Acc rprev[2][3];  // row low-pass of the previous two PAN rows, half-cols j-1, j, j+1
+  Acc pa[2][4];     // PAN rows 2i, 2i+1 at this thread's 4 columns
+  Acc ep[NB][3];    // E(i-1) at half-cols j-1, j, j+1
+
+  for (int n = 0; n < nloads; ++n) {
+    const int s = n % S;
+    tma::mbar_wait(&full[s], (n / S) & 1);
+    const T* slot = slots + (size_t)s * SLOT;
+    Acc v[2][8];  // PAN cols c-2 .. c+5 of the slot's two rows
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const T* pr = slot + q * PROW + 4 + rel;
+      lds2(pr - 2, v[q][0], v[q][1]);
+      lds2(pr, v[q][2], v[q][3]);
+      lds2(pr + 2, v[q][4], v[q][5]);
+      lds2(pr + 4, v[q][6], v[q][7]);
+    }
+    Acc m[NB][3];
+    if (n >= 1) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const T* mr = slot + 2 * PROW + b * MROW + 4 + (rel >> 1);
+        m[b][0] = mr[-1];
+        lds2(mr, m[b][1], m[b][2]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
+
+    Acc rn[2][3];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      rn[q][0] = dot4t(h0, h1, h2, h3, v[q][0], v[q][1], v[q][2], v[q][3]);
+      rn[q][1] = dot4t(h0, h1, h2, h3, v[q][2], v[q][3], v[q][4], v[q][5]);
+      rn[q][2] = dot4t(h0, h1, h2, h3, v[q][4], v[q][5], v[q][6], v[q][7]);
+    }
+    if (n >= 1) {
+      Acc ll[3];
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj)
+        ll[jj] = dot4t(h0, h1, h2, h3, rprev[0][jj], rprev[1][jj], rn[0][jj], rn[1][jj]);
+      if (n == 1) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = m[b][jj] + m[b][jj] - ll[jj];
+      } else {
+        const int i = i0 + n - 2;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          Acc e[3];
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) e[jj] = m[b][jj] + m[b][jj] - ll[jj];
+          if (valid) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              const Acc wp = p == 0 ? h2 : h3;
+              const Acc wc = p == 0 ? h0 : h1;
+              const Acc vm = fma(wc, e[0], wp * ep[b][0]);
+              const Acc v0 = fma(wc, e[1], wp * ep[b][1]);
+              const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
+              Acc o[4];
+              o[0] = pa[p][0] + fma(h0, v0, h2 * vm);
+              o[1] = pa[p][1] + fma(h1, v0, h3 * vm);
+              o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
+              o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
+              store4_vec<Acc>(a.out[b] + (long long)(2 * i + p) * a.out_pitch + c, o);
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = e[jj];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pa[q][k] = v[q][2 + k];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj) rprev[q][jj] = rn[q][jj];
+  }
+}
+
+template <typename T, int NB, int NCW>
+static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const LaunchTuning& tune) {
+  FuseArgs<T> a = a0;
+  constexpr int CW = 128 * NCW;
+  constexpr int SLOT = 2 * (CW + 8) + NB * (CW / 2 + 4);
+  const int npairs = a.rows >> 1;
+  int S = tune.d4_stages > 0 ? tune.d4_stages : 0;
+  if (S <= 0) {
+    // ~44 KB of ring per CTA: 4-5 CTAs per SM, >100 KB of reads in flight
+    S = (int)((44 * 1024) / (SLOT * sizeof(T)));
+    if (S < 2) S = 2;
+    if (S > 8) S = 8;
+  }
+  const size_t smem = (size_t)S * SLOT * sizeof(T) + 2 * S * sizeof(uint64_t);
+  auto kern = fuse_d4_tma_kernel<T, NB, NCW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  a.n_colbands = (a.W + CW - 1) / CW;
+  int P = tune.d4_pairs > 0 ? tune.d4_pairs : 8;  // measured best on Landsat (tools/sweep_d4.py)
+  if (P > npairs) P = npairs;
+  a.pairs_per_task = P;
+  const long long n_row = (npairs + P - 1) / P;
+  a.n_tasks = n_row * a.n_colbands;
+  kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune) {
+  switch (a.nbands) {
+    case 1: return launch_tma_nb<T, 1, 4>(a, s, tune);
+    case 2: return launch_tma_nb<T, 2, 4>(a, s, tune);
+    case 3: return launch_tma_nb<T, 3, 4>(a, s, tune);
+    case 4: return launch_tma_nb<T, 4, 4>(a, s, tune);
+    case 5: return launch_tma_nb<T, 5, 4>(a, s, tune);
+    case 6: return launch_tma_nb<T, 6, 4>(a, s, tune);
+    case 7: return launch_tma_nb<T, 7, 4>(a, s, tune);
+    case 8: return launch_tma_nb<T, 8, 4>(a, s, tune);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template cudaError_t launch_fuse_d4_tma<float>(const FuseArgs<float>&, cudaStream_t,
+                                               const LaunchTuning&);
+template cudaError_t launch_fuse_d4_tma<double>(const FuseArgs<double>&, cudaStream_t,
+                                                const LaunchTuning&);
+
+}  // namespace wf

@@ -53,21 +53,21 @@ __host__ __device__ inline D4 d4_taps() {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
   return r;
 }
 __device__ __forceinline__ float2 ld_stream(const float2* p) {
   float2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
                : "=f"(r.x), "=f"(r.y)
                : "l"(p));
   return r;
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
                : "=d"(r.x), "=d"(r.y)
                : "l"(p));
   return r;

@@ -38,11 +38,17 @@ struct FuseArgs {
 struct LaunchTuning {
   int d4_target_warps;  // <=0: occupancy x SMs
   int d4_min_pairs;     // <=0: no minimum
+  int d4_pairs;         // >0: fixed row pairs per warp task (overrides the above)
+  int d4_stages;        // >0: shared-memory ring depth of the TMA kernel
 };
 
+// vec: 16-byte vector path legal; tma: the bulk-copy D4 pipeline is legal
+// (W % 8 == 0, every row 16-byte aligned).
 template <typename T, typename Acc>
-cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, cudaStream_t s,
+cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, bool tma, cudaStream_t s,
                         const LaunchTuning& tune);
+template <typename T>
+cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune);
 
 // Standalone transforms (materialise coefficients; wavelet.py:131-164).
 template <typename T>
