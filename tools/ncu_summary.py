@@ -1,0 +1,60 @@
+"""Summarise an ncu --set full report into profiles/ (json + markdown).
+
+    python tools/ncu_summary.py gpurun_out/prof_r1.ncu-rep r01
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+        "launch__block_size", "smsp__inst_executed.sum", "lts__t_bytes.sum",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers"]
+SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1e-3, "us": 1e-6,
+         "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9, "ns": 1e-9}
+
+
+def main(rep, tag):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    out, md = {}, [f"# ncu --set full summary ({tag})", "",
+                   "| kernel | duration | DRAM read | DRAM write | DRAM % of ncu peak | "
+                   "SM % | regs | warps active % |", "|---|---|---|---|---|---|---|---|"]
+    seen = {}
+    for r in data:
+        name = r[hdr.index("Kernel Name")]
+        rec = {}
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                v = float(r[i].replace(",", "")) if r[i] else None
+                rec[k] = v * SCALE.get(units[i], 1) if v is not None else None
+        short = name.split("(")[0].replace("void ", "")
+        nb = short.split(",")[2].strip() if "haar" in short else short.split(",")[1].strip()
+        key = ("fuse_haar" if "haar" in short else "fuse_daub4") + f"_b{nb}"
+        seen[key] = seen.get(key, 0) + 1
+        rec["dram_bytes"] = rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
+        rec["kernel"] = short
+        out[key] = rec
+        md.append(f"| `{short}` | {rec['gpu__time_duration.sum'] * 1e3:.3f} ms | "
+                  f"{rec['dram__bytes_read.sum'] / 1e9:.3f} GB | "
+                  f"{rec['dram__bytes_write.sum'] / 1e9:.3f} GB | "
+                  f"{rec['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
+                  f"{rec['sm__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
+                  f"{rec['launch__registers_per_thread']:.0f} | "
+                  f"{rec['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} |")
+    (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
+    (ROOT / "profiles" / f"{tag}_ncu_summary.md").write_text("\n".join(md) + "\n")
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
