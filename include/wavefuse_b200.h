@@ -140,6 +140,34 @@ int wf_resample_bilinear_f64(const double* in, int64_t in_pitch, int in_h, int i
                              double* out, int64_t out_pitch, int out_h, int out_w,
                              void* stream);
 
+/* metrics.py:122-123 upsamples the float64-cast bands (_as_bands): float32
+ * source, float64 result, bit-identical to resample_bilinear(b.astype(f64)). */
+int wf_resample_bilinear_f32_to_f64(const float* in, int64_t in_pitch, int in_h, int in_w,
+                                    double* out, int64_t out_pitch, int out_h, int out_w,
+                                    void* stream);
+
+/* ---- quality metrics (metrics.py) --------------------------------------- */
+/* Planes are float32 (x_f64 = 0) or float64 (x_f64 = 1); all statistics are
+ * float64. Results land in DEVICE memory (out[out_index]); workspaces are
+ * caller-owned device scratch of the size the *_workspace_bytes call returns,
+ * so concurrent callers never share state. */
+int64_t wf_q_index_workspace_bytes(int h, int w);
+/* metrics.py:57-83 q_index(a, b): 32x32 blocks (partial edges dropped, planes
+ * under 32 are one block), population moments, den == 0 -> 1 if identical
+ * else 0; block mean. */
+int wf_q_index(const void* a, int a_f64, int64_t a_pitch, const void* b, int b_f64,
+               int64_t b_pitch, int h, int w, void* workspace, double* out, int out_index,
+               void* stream);
+/* metrics.py:31-42 degrade(plane, factor) -> float64 (h/f x w/f). */
+int wf_degrade(const void* in, int in_f64, int64_t in_pitch, int h, int w, int factor,
+               double* out, int64_t out_pitch, void* stream);
+int64_t wf_ergas_workspace_bytes(int rh, int rw);
+/* metrics.py:112-118, one band: out2[0] = mean((degrade(fused, ratio) - ref)^2),
+ * out2[1] = mean(ref). */
+int wf_ergas_band(const void* fused, int f_f64, int64_t f_pitch, const void* ref, int r_f64,
+                  int64_t r_pitch, int rh, int rw, int ratio, void* workspace, double* out2,
+                  void* stream);
+
 /* ---- synthetic scenes (counter hash; numpy twin in synth.py) ------------ */
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
                        uint32_t plane, int row0, int col0, void* stream);

@@ -22,6 +22,7 @@ from .errors import (
     ZeroBandMean,
 )
 from .fusion import DwtReplace, FusionMethod, fuse, fuse_dwt, method_from_name, resample_bilinear
+from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, q_index, qnr
 from .wavelet import (
     FilterBank,
     WaveletKind,
@@ -45,6 +46,7 @@ __all__ = [
     "NotDivisible",
     "OddDimension",
     "OddLength",
+    "QualityReport",
     "TooFewBands",
     "TooShort",
     "TooSmall",
@@ -52,12 +54,18 @@ __all__ = [
     "ZeroBandMean",
     "__version__",
     "d4_filters",
+    "d_lambda",
+    "d_s",
+    "degrade",
     "dwt1d_forward",
     "dwt1d_inverse",
     "dwt2d_forward",
     "dwt2d_inverse",
+    "ergas",
     "fuse",
     "fuse_dwt",
     "method_from_name",
+    "q_index",
+    "qnr",
     "resample_bilinear",
 ]

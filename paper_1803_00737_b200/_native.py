@@ -77,10 +77,21 @@ def _declare(lib: ctypes.CDLL) -> None:
 
 
 def _declare_quality(lib: ctypes.CDLL) -> None:
-    if not hasattr(lib, "wf_q_index_f64"):
-        return
-    lib.wf_q_index_f64.argtypes = [c_vp, c_vp, c_i64, c_int, c_int, ctypes.POINTER(ctypes.c_double), c_vp]
-    lib.wf_q_index_f64.restype = c_int
+    sig = {
+        "wf_resample_bilinear_f32_to_f64": ([c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_int, c_int,
+                                             c_vp], c_int),
+        "wf_q_index_workspace_bytes": ([c_int, c_int], c_i64),
+        "wf_q_index": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_int, c_int, c_vp, c_vp, c_int,
+                        c_vp], c_int),
+        "wf_degrade": ([c_vp, c_int, c_i64, c_int, c_int, c_int, c_vp, c_i64, c_vp], c_int),
+        "wf_ergas_workspace_bytes": ([c_int, c_int], c_i64),
+        "wf_ergas_band": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_int, c_int, c_int, c_vp,
+                           c_vp, c_vp], c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
 
 
 def load() -> ctypes.CDLL:

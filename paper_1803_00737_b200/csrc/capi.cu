@@ -386,13 +386,74 @@ WF_ROWS(wf_dwt_rows_inverse_f64, double, true)
       return fail(WF_ERR_VALUE, "output size %dx%d must be positive", out_w, out_h);        \
     if (in_w < 1 || in_h < 1) return fail(WF_ERR_VALUE, "empty input plane");              \
     if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");                    \
-    cudaError_t e = wf::launch_resample<T>(in, in_pitch, in_h, in_w, out, out_pitch, out_h, \
+    cudaError_t e = wf::launch_resample<T, T>(in, in_pitch, in_h, in_w, out, out_pitch, out_h, \
                                            out_w, (cudaStream_t)stream);                    \
     if (e == cudaSuccess) ++g_launches;                                                     \
     return cuda_status(e, #NAME);                                                           \
   }
 WF_RESAMPLE(wf_resample_bilinear_f32, float)
 WF_RESAMPLE(wf_resample_bilinear_f64, double)
+
+int wf_resample_bilinear_f32_to_f64(const float* in, int64_t in_pitch, int in_h, int in_w,
+                                     double* out, int64_t out_pitch, int out_h, int out_w,
+                                     void* stream) {
+  if (out_w < 1 || out_h < 1)
+    return fail(WF_ERR_VALUE, "output size %dx%d must be positive", out_w, out_h);
+  if (in_w < 1 || in_h < 1) return fail(WF_ERR_VALUE, "empty input plane");
+  if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");
+  cudaError_t e = wf::launch_resample<float, double>(in, in_pitch, in_h, in_w, out, out_pitch,
+                                                     out_h, out_w, (cudaStream_t)stream);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e, "wf_resample_bilinear_f32_to_f64");
+}
+
+int64_t wf_q_index_workspace_bytes(int h, int w) {
+  int bh, bw, nbr, nbc;
+  wf::q_geometry(h, w, bh, bw, nbr, nbc);
+  return (int64_t)nbr * nbc * (int64_t)sizeof(double);
+}
+
+int wf_q_index(const void* a, int a_f64, int64_t a_pitch, const void* b, int b_f64,
+               int64_t b_pitch, int h, int w, void* workspace, double* out, int out_index,
+               void* stream) {
+  if (!a || !b || !workspace || !out) return fail(WF_ERR_VALUE, "null pointer argument");
+  if (h < 1 || w < 1) return fail(WF_ERR_VALUE, "empty plane %dx%d", w, h);
+  cudaError_t e = wf::launch_q_index(a, a_f64, a_pitch, b, b_f64, b_pitch, h, w,
+                                     static_cast<double*>(workspace), out, out_index,
+                                     (cudaStream_t)stream);
+  if (e == cudaSuccess) g_launches += 2;
+  return cuda_status(e, "wf_q_index");
+}
+
+int wf_degrade(const void* in, int in_f64, int64_t in_pitch, int h, int w, int factor,
+               double* out, int64_t out_pitch, void* stream) {
+  if (factor < 1) return fail(WF_ERR_VALUE, "factor %d must be >= 1", factor);
+  if (h % factor || w % factor)
+    return fail(WF_ERR_NOT_DIVISIBLE, "%dx%d not divisible by %d", w, h, factor);
+  if (!in || !out) return fail(WF_ERR_VALUE, "null pointer argument");
+  if (h == 0 || w == 0) return WF_OK;
+  cudaError_t e = wf::launch_degrade(in, in_f64, in_pitch, h, w, factor, out, out_pitch,
+                                     (cudaStream_t)stream);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e, "wf_degrade");
+}
+
+int64_t wf_ergas_workspace_bytes(int rh, int rw) {
+  return 2 * (int64_t)wf::ergas_parts((long long)rh * rw) * (int64_t)sizeof(double);
+}
+
+int wf_ergas_band(const void* fused, int f_f64, int64_t f_pitch, const void* ref, int r_f64,
+                  int64_t r_pitch, int rh, int rw, int ratio, void* workspace, double* out2,
+                  void* stream) {
+  if (!fused || !ref || !workspace || !out2) return fail(WF_ERR_VALUE, "null pointer argument");
+  if (ratio < 1) return fail(WF_ERR_VALUE, "ratio %d must be >= 1", ratio);
+  if (rh < 1 || rw < 1) return fail(WF_ERR_VALUE, "empty reference band");
+  cudaError_t e = wf::launch_ergas_band(fused, f_f64, f_pitch, ref, r_f64, r_pitch, rh, rw,
+                                        ratio, static_cast<double*>(workspace), out2,
+                                        (cudaStream_t)stream);
+  if (e == cudaSuccess) g_launches += 2;
+  return cuda_status(e, "wf_ergas_band");
+}
 
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
                        uint32_t plane, int row0, int col0, void* stream) {

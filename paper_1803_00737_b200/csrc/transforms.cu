@@ -148,9 +148,9 @@ __device__ __forceinline__ void src_coord(int dst, int in_n, int out_n, int& i0,
   f = sub(s, fl);
 }
 
-template <typename T>
+template <typename T, typename To>
 __global__ void resample_kernel(const T* __restrict__ in, long long ip, int in_h, int in_w,
-                                T* __restrict__ out, long long op, int out_h, int out_w) {
+                                To* __restrict__ out, long long op, int out_h, int out_w) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= out_w || y >= out_h) return;
@@ -163,7 +163,7 @@ __global__ void resample_kernel(const T* __restrict__ in, long long ip, int in_h
   const double gx = sub(1.0, fx), gy = sub(1.0, fy);
   const double ru = add(mul((double)up[x0], gx), mul((double)up[x1], fx));
   const double rl = add(mul((double)lo[x0], gx), mul((double)lo[x1], fx));
-  out[(long long)y * op + x] = (T)add(mul(ru, gy), mul(rl, fy));
+  out[(long long)y * op + x] = (To)add(mul(ru, gy), mul(rl, fy));
 }
 
 // ---- counter-hash synthetic planes -----------------------------------------
@@ -221,12 +221,12 @@ cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long ip, T
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_resample(const T* in, long long ip, int in_h, int in_w, T* out, long long op,
+template <typename T, typename To>
+cudaError_t launch_resample(const T* in, long long ip, int in_h, int in_w, To* out, long long op,
                             int out_h, int out_w, cudaStream_t s) {
   dim3 block(32, 8);
   dim3 grid((out_w + 31) / 32, (out_h + 7) / 8);
-  resample_kernel<T><<<grid, block, 0, s>>>(in, ip, in_h, in_w, out, op, out_h, out_w);
+  resample_kernel<T, To><<<grid, block, 0, s>>>(in, ip, in_h, in_w, out, op, out_h, out_w);
   return cudaGetLastError();
 }
 
@@ -245,9 +245,11 @@ template cudaError_t launch_dwt_rows<float>(int, bool, const float*, long long, 
                                             long long, int, int, cudaStream_t);
 template cudaError_t launch_dwt_rows<double>(int, bool, const double*, long long, double*,
                                              long long, int, int, cudaStream_t);
-template cudaError_t launch_resample<float>(const float*, long long, int, int, float*, long long,
-                                            int, int, cudaStream_t);
-template cudaError_t launch_resample<double>(const double*, long long, int, int, double*,
-                                             long long, int, int, cudaStream_t);
+template cudaError_t launch_resample<float, float>(const float*, long long, int, int, float*,
+                                                   long long, int, int, cudaStream_t);
+template cudaError_t launch_resample<double, double>(const double*, long long, int, int, double*,
+                                                     long long, int, int, cudaStream_t);
+template cudaError_t launch_resample<float, double>(const float*, long long, int, int, double*,
+                                                    long long, int, int, cudaStream_t);
 
 }  // namespace wf

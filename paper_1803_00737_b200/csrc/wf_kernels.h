@@ -59,9 +59,21 @@ cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long in_pi
                             long long out_pitch, int nrows, int n, cudaStream_t s);
 
 // fusion.py:50-81
-template <typename T>
-cudaError_t launch_resample(const T* in, long long in_pitch, int in_h, int in_w, T* out,
+template <typename T, typename To>
+cudaError_t launch_resample(const T* in, long long in_pitch, int in_h, int in_w, To* out,
                             long long out_pitch, int out_h, int out_w, cudaStream_t s);
+
+// Quality metrics (metrics.py). `*64` flags: 1 = the plane is float64, 0 = float32.
+void q_geometry(int h, int w, int& bh, int& bw, int& nbr, int& nbc);
+cudaError_t launch_q_index(const void* a, int a64, long long ap, const void* b, int b64,
+                           long long bp, int h, int w, double* scratch, double* out,
+                           int out_index, cudaStream_t s);
+cudaError_t launch_degrade(const void* in, int in64, long long ip, int h, int w, int f,
+                           double* out, long long op, cudaStream_t s);
+int ergas_parts(long long n);
+cudaError_t launch_ergas_band(const void* fz, int f64, long long fp, const void* rf, int r64,
+                              long long rp, int rh, int rw, int f, double* scratch, double* out,
+                              cudaStream_t s);
 
 // Counter-hash synthetic plane (uniform [0,255) f32), numpy twin in
 // paper_1803_00737_b200/synth.py.

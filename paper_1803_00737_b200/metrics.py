@@ -1,0 +1,296 @@
+"""Fusion quality metrics on the GPU: degrade, Q-index, ERGAS, D_lambda, D_s,
+QNR.
+
+Drop-in for /root/reference/pkg/src/wavefuse/metrics.py (same names,
+signatures, validation order and exception classes). All statistics are
+float64 on the device (csrc/quality.cu): two-pass block moments per 32x32 Q
+block with the reference's degenerate rule, deterministic reductions. Planes
+may be numpy arrays or CUDA tensors (float32 planes are read as float32 and
+widened exactly in-kernel, so no float64 copy of a fused scene is made).
+Scalars come back to the host once per public call.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .errors import DimensionMismatch, NotDivisible, TooFewBands, ZeroBandMean
+
+BLOCK = 32  # metrics.py:17
+
+
+@dataclass(frozen=True)
+class QualityReport:
+    """metrics.py:20-28"""
+
+    ergas: float
+    q_per_band: list[float]
+    d_lambda: float
+    d_s: float
+    qnr: float
+
+
+# ---------------------------------------------------------------- plumbing --
+def _shape(x):
+    return tuple(x.shape) if isinstance(x, torch.Tensor) else np.shape(x)
+
+
+def _plane(x) -> torch.Tensor:
+    """Contiguous CUDA tensor, float32 kept as float32, everything else
+    float64 (the reference casts everything to float64, metrics.py:86-91;
+    float32 -> float64 is exact and happens in-kernel)."""
+    dt = np.float32 if _device.is_f32(x) else np.float64
+    return _device.to_device(x, dt)
+
+
+def _is64(t: torch.Tensor) -> int:
+    return 1 if t.dtype == torch.float64 else 0
+
+
+def _bands(image) -> list:
+    """metrics.py:86-91: list of planes, all the same shape."""
+    bands = [b if isinstance(b, torch.Tensor) else np.asarray(b) for b in image]
+    for b in bands[1:]:
+        if _shape(b) != _shape(bands[0]):
+            raise DimensionMismatch(f"band sizes differ: {_shape(b)} vs {_shape(bands[0])}")
+    return bands
+
+
+class _Results:
+    """A device float64 vector the kernels write scalars into; read once."""
+
+    def __init__(self, n: int, device):
+        self.t = torch.zeros(max(1, n), dtype=torch.float64, device=device)
+        self.n = 0
+
+    def slot(self) -> int:
+        self.n += 1
+        return self.n - 1
+
+    def host(self) -> np.ndarray:
+        return self.t.cpu().numpy()
+
+
+def _q_into(res: _Results, a: torch.Tensor, b: torch.Tensor) -> int:
+    h, w = a.shape
+    lib = _native.load()
+    ws = torch.empty(int(lib.wf_q_index_workspace_bytes(h, w)) // 8 + 1, dtype=torch.float64,
+                     device=a.device)
+    idx = res.slot()
+    _native.check(lib.wf_q_index(a.data_ptr(), _is64(a), a.stride(0), b.data_ptr(), _is64(b),
+                                 b.stride(0), h, w, ws.data_ptr(), res.t.data_ptr(), idx,
+                                 _device.stream_ptr()))
+    return idx
+
+
+def _degrade_dev(p: torch.Tensor, factor: int) -> torch.Tensor:
+    h, w = p.shape
+    out = torch.empty((h // factor, w // factor), dtype=torch.float64, device=p.device)
+    _native.check(_native.load().wf_degrade(p.data_ptr(), _is64(p), p.stride(0), h, w, factor,
+                                            out.data_ptr(), out.stride(0), _device.stream_ptr()))
+    return out
+
+
+def _upsample_dev(b: torch.Tensor, w: int, h: int) -> torch.Tensor:
+    """metrics.py:122-123 on a float64-cast band: bit-identical to the
+    reference's resample_bilinear(band.astype(float64), w, h)."""
+    if tuple(b.shape) == (h, w):
+        return b
+    lib = _native.load()
+    out = torch.empty((h, w), dtype=torch.float64, device=b.device)
+    bh, bw = b.shape
+    fn = lib.wf_resample_bilinear_f64 if b.dtype == torch.float64 else lib.wf_resample_bilinear_f32_to_f64
+    _native.check(fn(b.data_ptr(), b.stride(0), bh, bw, out.data_ptr(), w, h, w,
+                     _device.stream_ptr()))
+    return out
+
+
+# ------------------------------------------------------------ public API ---
+def degrade(plane, factor: int):
+    """metrics.py:31-42: factor x factor block mean, float64."""
+    if factor < 1:
+        raise ValueError(f"factor {factor} must be >= 1")
+    shape = _shape(plane)
+    if factor == 1:
+        if isinstance(plane, torch.Tensor):
+            return plane.to(torch.float64).clone()
+        return np.array(plane, dtype=np.float64, copy=True)
+    h, w = shape
+    if h % factor or w % factor:
+        raise NotDivisible(f"{w}x{h} not divisible by {factor}")
+    out = _degrade_dev(_plane(plane), factor)
+    return out if isinstance(plane, torch.Tensor) else out.cpu().numpy()
+
+
+def q_index(a, b) -> float:
+    """metrics.py:57-83: block-averaged universal image quality index."""
+    if _shape(a) != _shape(b):
+        raise DimensionMismatch(f"planes differ: {_shape(a)} vs {_shape(b)}")
+    ta, tb = _plane(a), _plane(b)
+    res = _Results(1, ta.device)
+    _q_into(res, ta, tb)
+    return float(res.host()[0])
+
+
+def _ergas_checks(f_bands, r_bands, ratio):
+    if ratio < 1:
+        raise ValueError(f"ratio {ratio} must be >= 1")
+    if len(f_bands) != len(r_bands):
+        raise DimensionMismatch(f"band counts differ: {len(f_bands)} vs {len(r_bands)}")
+    rh, rw = _shape(r_bands[0])
+    if _shape(f_bands[0]) != (rh * ratio, rw * ratio):
+        raise DimensionMismatch(
+            f"fused {_shape(f_bands[0])} is not reference {_shape(r_bands[0])} times {ratio}"
+        )
+
+
+def _ergas_into(res: _Results, f_t, r_t, ratio) -> list[int]:
+    lib = _native.load()
+    rh, rw = r_t[0].shape
+    ws = torch.empty(int(lib.wf_ergas_workspace_bytes(rh, rw)) // 8 + 1, dtype=torch.float64,
+                     device=r_t[0].device)
+    slots = []
+    for fb, rb in zip(f_t, r_t):
+        i0 = res.slot()
+        res.slot()
+        _native.check(lib.wf_ergas_band(fb.data_ptr(), _is64(fb), fb.stride(0), rb.data_ptr(),
+                                        _is64(rb), rb.stride(0), rh, rw, ratio, ws.data_ptr(),
+                                        res.t.data_ptr() + 8 * i0, _device.stream_ptr()))
+        slots.append(i0)
+    return slots
+
+
+def _ergas_value(vals: np.ndarray, slots: list[int], ratio: int) -> float:
+    acc = 0.0
+    for i0 in slots:
+        mse, mu = float(vals[i0]), float(vals[i0 + 1])
+        if mu == 0.0:
+            raise ZeroBandMean("reference band mean is zero")
+        acc += mse / (mu * mu)
+    return 100.0 / ratio * float(np.sqrt(acc / len(slots)))
+
+
+def ergas(fused, ms_ref, ratio: int) -> float:
+    """metrics.py:94-119"""
+    if ratio < 1:
+        raise ValueError(f"ratio {ratio} must be >= 1")
+    f_bands, r_bands = _bands(fused), _bands(ms_ref)
+    _ergas_checks(f_bands, r_bands, ratio)
+    f_t = [_plane(b) for b in f_bands]
+    r_t = [_plane(b) for b in r_bands]
+    res = _Results(2 * len(f_t), f_t[0].device)
+    slots = _ergas_into(res, f_t, r_t, ratio)
+    return _ergas_value(res.host(), slots, ratio)
+
+
+def _dlambda_checks(f_bands, m_bands):
+    n = len(f_bands)
+    if n != len(m_bands):
+        raise DimensionMismatch(f"band counts differ: {n} vs {len(m_bands)}")
+    if n < 2:
+        raise TooFewBands("inter-band comparison needs at least 2 bands")
+
+
+def _dlambda_into(res, f_t, up_t) -> list[tuple[int, int]]:
+    n = len(f_t)
+    return [(_q_into(res, f_t[k], f_t[l]), _q_into(res, up_t[k], up_t[l]))
+            for k in range(n) for l in range(k + 1, n)]
+
+
+def _dlambda_value(vals, pairs, n) -> float:
+    total = 0.0
+    for i, j in pairs:
+        total += 2.0 * abs(float(vals[i]) - float(vals[j]))
+    return min(1.0, max(0.0, total / (n * (n - 1))))
+
+
+def d_lambda(fused, ms) -> float:
+    """metrics.py:126-142: spectral distortion."""
+    f_bands, m_bands = _bands(fused), _bands(ms)
+    _dlambda_checks(f_bands, m_bands)
+    f_t = [_plane(b) for b in f_bands]
+    fh, fw = f_t[0].shape
+    up_t = [_upsample_dev(_plane(b), fw, fh) for b in m_bands]
+    n = len(f_t)
+    res = _Results(n * (n - 1), f_t[0].device)
+    pairs = _dlambda_into(res, f_t, up_t)
+    return _dlambda_value(res.host(), pairs, n)
+
+
+def _infer_ratio(pan_shape, ms_shape) -> int:
+    """metrics.py:145-152"""
+    ph, pw = pan_shape
+    mh, mw = ms_shape
+    if mh == 0 or mw == 0 or ph % mh or pw % mw or ph // mh != pw // mw:
+        raise DimensionMismatch(
+            f"panchromatic {tuple(pan_shape)} is not an integer multiple of bands {tuple(ms_shape)}"
+        )
+    return ph // mh
+
+
+def _ds_checks(f_bands, m_bands, pan) -> int:
+    if len(f_bands) != len(m_bands):
+        raise DimensionMismatch(f"band counts differ: {len(f_bands)} vs {len(m_bands)}")
+    if _shape(f_bands[0]) != _shape(pan):
+        raise DimensionMismatch(
+            f"fused {_shape(f_bands[0])} does not match panchromatic {_shape(pan)}"
+        )
+    return _infer_ratio(_shape(pan), _shape(m_bands[0]))
+
+
+def _ds_into(res, f_t, m_t, p_t, ratio):
+    low = _degrade_dev(p_t, ratio) if ratio != 1 else p_t
+    return [(_q_into(res, fb, p_t), _q_into(res, mb, low)) for fb, mb in zip(f_t, m_t)]
+
+
+def _ds_value(vals, pairs) -> float:
+    total = sum(abs(float(vals[i]) - float(vals[j])) for i, j in pairs)
+    return min(1.0, max(0.0, total / len(pairs)))
+
+
+def d_s(fused, ms, pan) -> float:
+    """metrics.py:155-175: spatial distortion."""
+    f_bands, m_bands = _bands(fused), _bands(ms)
+    ratio = _ds_checks(f_bands, m_bands, pan)
+    f_t = [_plane(b) for b in f_bands]
+    m_t = [_plane(b) for b in m_bands]
+    p_t = _plane(pan)
+    res = _Results(2 * len(f_t), p_t.device)
+    pairs = _ds_into(res, f_t, m_t, p_t, ratio)
+    return _ds_value(res.host(), pairs)
+
+
+def qnr(fused, ms, pan) -> QualityReport:
+    """metrics.py:178-199: the full report. All preconditions are checked
+    before any compute; every Q, MSE and mean is computed on the GPU and the
+    scalars are read back once."""
+    f_bands, m_bands = _bands(fused), _bands(ms)
+    ratio = _infer_ratio(_shape(pan), _shape(m_bands[0]))
+    _dlambda_checks(f_bands, m_bands)
+    _ds_checks(f_bands, m_bands, pan)
+    _ergas_checks(f_bands, m_bands, ratio)
+    f_t = [_plane(b) for b in f_bands]
+    m_t = [_plane(b) for b in m_bands]
+    p_t = _plane(pan)
+    fh, fw = f_t[0].shape
+    up_t = [_upsample_dev(b, fw, fh) for b in m_t]
+    n = len(f_t)
+    res = _Results(n + n * (n - 1) + 2 * n + 2 * n, p_t.device)
+    per_band = [_q_into(res, fb, ub) for fb, ub in zip(f_t, up_t)]
+    dl_pairs = _dlambda_into(res, f_t, up_t)
+    ds_pairs = _ds_into(res, f_t, m_t, p_t, ratio)
+    e_slots = _ergas_into(res, f_t, m_t, ratio)
+    vals = res.host()
+    spectral = _dlambda_value(vals, dl_pairs, n)
+    spatial = _ds_value(vals, ds_pairs)
+    return QualityReport(
+        ergas=_ergas_value(vals, e_slots, ratio),
+        q_per_band=[float(vals[i]) for i in per_band],
+        d_lambda=spectral,
+        d_s=spatial,
+        qnr=(1.0 - spectral) * (1.0 - spatial),
+    )

@@ -1,0 +1,119 @@
+"""Multi-GPU drivers (north-star subsystem (c)).
+
+* Scenes and bands are independent units: `shard` assigns them round-robin to
+  ranks; no collective on the data path.
+* One scene too large for one GPU is cut into row strips, one per rank
+  (`strip_bounds`). Haar needs no halo (2x2-local). D4 output
+  rows {2i, 2i+1} need PAN rows 2i-2..2i+3 and MS rows i-1, i with global
+  periodic wrap (F3), so rank g needs the last 2 PAN rows and the last MS row
+  of every band of rank g-1, and the first 2 PAN rows of rank g+1 (rank 0 and
+  rank P-1 are neighbours). `exchange_halos` moves exactly those rows with one
+  batched ring of point-to-point sends/receives (NCCL over NVLink on the GPU
+  box; gloo in the CPU tests), then `wf_fuse_strip_*` fuses the strip with the
+  halo rows as separate buffers. Results equal the untiled fusion bit for bit
+  (the reference's tiled D4, tiling.py:1-12, instead wraps per tile and
+  differs in a 2-px border band).
+
+Halo volume per rank: 4 PAN rows + B MS rows, e.g. 1.1 MiB at W = 65536 —
+<0.03% of a 8192-row strip's traffic.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _device, _native
+from .wavelet import KIND_CODE, WaveletKind
+
+
+def shard(items: Sequence, rank: int, world: int) -> list:
+    """Round-robin ownership of independent units (scenes, bands)."""
+    return [x for i, x in enumerate(items) if i % world == rank]
+
+
+def strip_bounds(h: int, world: int, rank: int, align: int = 64) -> tuple[int, int]:
+    """PAN rows [r0, r1) of `rank`'s strip. Boundaries are multiples of
+    `align` (even, and 64 keeps 32x32 Q blocks and their low-resolution
+    counterparts inside one rank); the last rank takes the remainder."""
+    step = (h // world) // align * align
+    if step < 2:
+        raise ValueError(f"{h} rows cannot be split into {world} strips of >= 2 rows")
+    r0 = rank * step
+    r1 = h if rank == world - 1 else r0 + step
+    return r0, r1
+
+
+def exchange_halos(pan: torch.Tensor, ms: list[torch.Tensor], group=None):
+    """Ring exchange of the D4 halo rows of this rank's strip.
+
+    Returns (pan_top[2, W], pan_bot[2, W], ms_top[b][1, W/2]): the 2 PAN rows
+    above the strip, the 2 PAN rows below it, and the MS row above it, with
+    the global periodic wrap (rank 0's top comes from the last rank).
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return (pan[-2:].contiguous(), pan[:2].contiguous(),
+                [m[-1:].contiguous() for m in ms])
+    rank = dist.get_rank(group)
+    prev, nxt = (rank - 1) % world, (rank + 1) % world
+    if group is not None:
+        prev = dist.get_global_rank(group, prev)
+        nxt = dist.get_global_rank(group, nxt)
+    w = pan.shape[1]
+    pan_top = torch.empty((2, w), dtype=pan.dtype, device=pan.device)
+    pan_bot = torch.empty((2, w), dtype=pan.dtype, device=pan.device)
+    ms_top = [torch.empty((1, m.shape[1]), dtype=m.dtype, device=m.device) for m in ms]
+    # order-consistent per peer: sends [last2, first2, ms_last...] match the
+    # peer's receives [top, bot, ms_top...]
+    last2, first2 = pan[-2:].contiguous(), pan[:2].contiguous()
+    ms_last = [m[-1:].contiguous() for m in ms]
+    ops = [dist.P2POp(dist.isend, last2, nxt, group),
+           dist.P2POp(dist.irecv, pan_top, prev, group),
+           dist.P2POp(dist.isend, first2, prev, group),
+           dist.P2POp(dist.irecv, pan_bot, nxt, group)]
+    for src, dst in zip(ms_last, ms_top):
+        ops.append(dist.P2POp(dist.isend, src, nxt, group))
+        ops.append(dist.P2POp(dist.irecv, dst, prev, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return pan_top, pan_bot, ms_top
+
+
+def fuse_strip(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
+               halos=None, out: list[torch.Tensor] | None = None) -> list[torch.Tensor]:
+    """Fuse one row strip on this rank's GPU through wf_fuse_strip_*.
+    `halos` = exchange_halos(...) result (required for D4)."""
+    rows, w = pan.shape
+    if out is None:
+        out = [torch.empty_like(pan) for _ in ms]
+    lib = _native.load()
+    fn = lib.wf_fuse_strip_f32 if pan.dtype == torch.float32 else lib.wf_fuse_strip_f64
+    if kind is WaveletKind.DAUB4:
+        top, bot, mtop = halos
+        top_p, bot_p = top.data_ptr(), bot.data_ptr()
+        mtop_p = _native.ptr_array([m.data_ptr() for m in mtop])
+        hp = top.stride(0)
+    else:
+        top_p = bot_p = None
+        mtop_p = None
+        hp = 0
+    _native.check(fn(KIND_CODE[kind], pan.data_ptr(), pan.stride(0), top_p, bot_p, hp,
+                     _native.ptr_array([m.data_ptr() for m in ms]), mtop_p, ms[0].stride(0),
+                     _native.ptr_array([o.data_ptr() for o in out]), out[0].stride(0), len(ms),
+                     rows, w, _device.stream_ptr()))
+    return out
+
+
+def fuse_scene_strips(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor], group=None,
+                      compute: Callable | None = None):
+    """This rank's share of a strip-sharded scene: halo exchange (D4 only),
+    then the strip kernel. `compute(kind, pan, ms, halos)` replaces the GPU
+    kernel in CPU-only tests of the exchange logic (tests inject the oracle);
+    the product path always uses the sm_100a kernel."""
+    halos = exchange_halos(pan, ms, group) if kind is WaveletKind.DAUB4 else None
+    if compute is not None:
+        return compute(kind, pan, ms, halos)
+    return fuse_strip(kind, pan, ms, halos)

@@ -341,3 +341,18 @@ def test_tma_and_register_paths_bit_identical(shape, monkeypatch):
     ref = O.fuse(pan.cpu().numpy(), [b.cpu().numpy() for b in bands], "daub4")
     for a, r in zip(fast, ref):
         assert _maxabs(a.cpu().numpy(), r) <= F32_TOL
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+def test_strip_driver_single_rank_equals_fuse(kname):
+    """strips.fuse_scene_strips at world size 1 (halo rows wrap locally)
+    equals the whole-scene fusion bit for bit."""
+    from paper_1803_00737_b200 import strips
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    pan = torch.rand((512, 1024), generator=g, device="cuda") * 255
+    ms = [torch.rand((256, 512), generator=g, device="cuda") * 255 for _ in range(2)]
+    got = strips.fuse_scene_strips(KINDS[kname], pan, ms)
+    want = wf.fuse(pan, ms, wf.DwtReplace(KINDS[kname]))
+    for a, b in zip(got, want):
+        assert torch.equal(a, b)
