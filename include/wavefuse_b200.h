@@ -21,9 +21,10 @@
  *   wf_dwt_rows_forward_*  wavelet.py:131-139  dwt1d_forward (nrows = 1)
  *   wf_dwt_rows_inverse_*  wavelet.py:142-146  dwt1d_inverse (nrows = 1)
  *   wf_resample_bilinear_* fusion.py:50-81     resample_bilinear(plane, w, h)
- *   wf_degrade_*           metrics.py:31-42    degrade(plane, factor)
- *   wf_q_index_*           metrics.py:45-83    q_index(a, b)
- *   wf_quality_scene_f32   metrics.py:94-199   qnr()/ergas() partials
+ *   wf_degrade             metrics.py:31-42    degrade(plane, factor)
+ *   wf_q_index             metrics.py:45-83    q_index(a, b)
+ *   wf_ergas_band          metrics.py:94-119   ergas() per band
+ *   wf_quality_scene_f32   metrics.py:178-199  qnr() in one pass over the scene
  *
  * Conventions
  *  - All array arguments of the device entry points are DEVICE pointers;
@@ -167,6 +168,23 @@ int64_t wf_ergas_workspace_bytes(int rh, int rw);
 int wf_ergas_band(const void* fused, int f_f64, int64_t f_pitch, const void* ref, int r_f64,
                   int64_t r_pitch, int rh, int rw, int ratio, void* workspace, double* out2,
                   void* stream);
+
+/* metrics.py:178-199 qnr() in ONE pass over a float32 scene (ratio 2,
+ * 2..8 bands, even H, W % 8 == 0, H, W >= 64, 16-byte aligned rows). out (device, float64):
+ *   [0, B)                 Q(F_k, U_k)            (q_per_band)
+ *   [B, B + B(B-1)/2)      Q(F_k, F_l), k < l     (d_lambda, fused side)
+ *   next B(B-1)/2          Q(U_k, U_l), k < l     (d_lambda, upsampled side)
+ *   next B                 Q(F_k, P)              (d_s, full resolution)
+ *   next B                 Q(M_k, degrade(P, 2))  (d_s, low resolution)
+ *   next B                 MSE(degrade(F_k, 2), M_k)   (ergas)
+ *   next B                 mean(M_k)                   (ergas)
+ * with U_k = resample_bilinear(M_k, W, H). *undecidable > 0 means some block
+ * hit den == 0 with non-constant data (the reference then compares the blocks
+ * element-wise): recompute with wf_q_index. */
+int64_t wf_quality_scene_workspace_bytes(int nbands, int h, int w);
+int wf_quality_scene_f32(const float* const* fused, const float* const* ms, const float* pan,
+                         int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
+                         int w, void* workspace, double* out, int* undecidable, void* stream);
 
 /* ---- synthetic scenes (counter hash; numpy twin in synth.py) ------------ */
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,

@@ -455,6 +455,37 @@ int wf_ergas_band(const void* fused, int f_f64, int64_t f_pitch, const void* ref
   return cuda_status(e, "wf_ergas_band");
 }
 
+int64_t wf_quality_scene_workspace_bytes(int nbands, int h, int w) {
+  return (int64_t)wf::quality_scene_workspace(nbands, h, w);
+}
+
+int wf_quality_scene_f32(const float* const* fused, const float* const* ms, const float* pan,
+                         int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
+                         int w, void* workspace, double* out, int* undecidable, void* stream) {
+  if (!fused || !ms || !pan || !workspace || !out || !undecidable)
+    return fail(WF_ERR_VALUE, "null pointer argument");
+  if (nbands < 2 || nbands > wf::kMaxBandsPerLaunch)
+    return fail(WF_ERR_BAND_COUNT, "fused quality path takes 2..%d bands, got %d",
+                wf::kMaxBandsPerLaunch, nbands);
+  if ((h & 1) || (w % 8) || h < 64 || w < 64)
+    return fail(WF_ERR_VALUE, "fused quality path needs even H, W % 8 == 0, H, W >= 64 (got %dx%d)",
+                w, h);
+  auto row16 = [](int64_t pitch) { return (pitch * 4) % 16 == 0; };
+  if (!row16(f_pitch) || !row16(pan_pitch) || !row16(ms_pitch) || !al16(pan) || f_pitch < w ||
+      pan_pitch < w || ms_pitch < w / 2)
+    return fail(WF_ERR_VALUE, "fused quality path needs 16-byte aligned rows");
+  for (int b = 0; b < nbands; ++b) {
+    if (!fused[b] || !ms[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
+    if (!al16(fused[b]) || !al16(ms[b]))
+      return fail(WF_ERR_VALUE, "band %d not 16-byte aligned", b);
+  }
+  cudaError_t e = wf::launch_quality_scene(nbands, fused, ms, pan, f_pitch, ms_pitch, pan_pitch,
+                                           h, w, workspace, out, undecidable,
+                                           (cudaStream_t)stream);
+  if (e == cudaSuccess) g_launches += 3;
+  return cuda_status(e, "wf_quality_scene_f32");
+}
+
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
                        uint32_t plane, int row0, int col0, void* stream) {
   if (!out || rows < 0 || cols < 0 || pitch < cols)

@@ -75,6 +75,14 @@ cudaError_t launch_ergas_band(const void* fz, int f64, long long fp, const void*
                               long long rp, int rh, int rw, int f, double* scratch, double* out,
                               cudaStream_t s);
 
+// Fused single-pass quality report (quality_scene.cu), float32 planes,
+// ratio 2, 2..8 bands, H, W >= 64.
+size_t quality_scene_workspace(int nb, int h, int w);
+cudaError_t launch_quality_scene(int nb, const float* const* F, const float* const* M,
+                                 const float* P, long long fp, long long mp, long long pp, int h,
+                                 int w, void* workspace, double* out, int* undecidable,
+                                 cudaStream_t s);
+
 // Counter-hash synthetic plane (uniform [0,255) f32), numpy twin in
 // paper_1803_00737_b200/synth.py.
 cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsigned long long seed,

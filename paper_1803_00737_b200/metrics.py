@@ -264,10 +264,60 @@ def d_s(fused, ms, pan) -> float:
     return _ds_value(res.host(), pairs)
 
 
+def _qnr_scene(f_t, m_t, p_t, ratio) -> QualityReport | None:
+    """One-pass fused report (csrc/quality_scene.cu) when the scene qualifies:
+    float32 planes, ratio 2, 2..8 bands, H, W >= 64. None = use the generic
+    path (also when a block needs the element-wise identity test)."""
+    import os
+
+    n = len(f_t)
+    h, w = p_t.shape
+    if (os.environ.get("WF_QNR_PATH") == "generic" or ratio != 2 or not 2 <= n <= 8
+            or h < 64 or w < 64 or w % 8
+            or any(t.dtype != torch.float32 for t in (*f_t, *m_t, p_t))
+            or any(t.data_ptr() % 16 for t in (*f_t, *m_t, p_t))):
+        return None
+    lib = _native.load()
+    ws = torch.empty(int(lib.wf_quality_scene_workspace_bytes(n, h, w)) // 8 + 1,
+                     dtype=torch.float64, device=p_t.device)
+    c = n * (n - 1) // 2
+    out = torch.zeros(n + 2 * c + 4 * n, dtype=torch.float64, device=p_t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=p_t.device)
+    _native.check(lib.wf_quality_scene_f32(
+        _native.ptr_array([t.data_ptr() for t in f_t]),
+        _native.ptr_array([t.data_ptr() for t in m_t]), p_t.data_ptr(), f_t[0].stride(0),
+        m_t[0].stride(0), p_t.stride(0), n, h, w, ws.data_ptr(), out.data_ptr(),
+        flag.data_ptr(), _device.stream_ptr()))
+    vals = out.cpu().numpy()
+    if int(flag.item()):
+        return None
+    fu = vals[:n]
+    ff, uu = vals[n:n + c], vals[n + c:n + 2 * c]
+    fp = vals[n + 2 * c:2 * n + 2 * c]
+    low = vals[2 * n + 2 * c:3 * n + 2 * c]
+    mse = vals[3 * n + 2 * c:4 * n + 2 * c]
+    mu = vals[4 * n + 2 * c:]
+    spectral = min(1.0, max(0.0, float(np.sum(2.0 * np.abs(ff - uu))) / (n * (n - 1))))
+    spatial = min(1.0, max(0.0, float(np.sum(np.abs(fp - low))) / n))
+    acc = 0.0
+    for k in range(n):
+        if mu[k] == 0.0:
+            raise ZeroBandMean("reference band mean is zero")
+        acc += float(mse[k]) / (float(mu[k]) * float(mu[k]))
+    return QualityReport(
+        ergas=100.0 / ratio * float(np.sqrt(acc / n)),
+        q_per_band=[float(v) for v in fu],
+        d_lambda=spectral,
+        d_s=spatial,
+        qnr=(1.0 - spectral) * (1.0 - spatial),
+    )
+
+
 def qnr(fused, ms, pan) -> QualityReport:
     """metrics.py:178-199: the full report. All preconditions are checked
     before any compute; every Q, MSE and mean is computed on the GPU and the
-    scalars are read back once."""
+    scalars are read back once. Float32 scenes at ratio 2 take the one-pass
+    scene kernel; anything else the per-pair kernels."""
     f_bands, m_bands = _bands(fused), _bands(ms)
     ratio = _infer_ratio(_shape(pan), _shape(m_bands[0]))
     _dlambda_checks(f_bands, m_bands)
@@ -276,6 +326,9 @@ def qnr(fused, ms, pan) -> QualityReport:
     f_t = [_plane(b) for b in f_bands]
     m_t = [_plane(b) for b in m_bands]
     p_t = _plane(pan)
+    fast = _qnr_scene(f_t, m_t, p_t, ratio)
+    if fast is not None:
+        return fast
     fh, fw = f_t[0].shape
     up_t = [_upsample_dev(b, fw, fh) for b in m_t]
     n = len(f_t)

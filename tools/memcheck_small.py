@@ -1,0 +1,37 @@
+"""Small-shape exercise of every kernel, for compute-sanitizer memcheck."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1803_00737_b200 as wf
+from paper_1803_00737_b200 import strips
+
+rng = np.random.default_rng(1)
+for (h, w, nb) in [(64, 1040, 6), (96, 200, 3), (8, 16, 2), (130, 264, 8), (6, 10, 1), (64, 64, 2)]:
+    pan = torch.from_numpy(rng.uniform(0, 255, (h, w)).astype(np.float32)).cuda()
+    ms = [torch.from_numpy(rng.uniform(1, 255, (h // 2, w // 2)).astype(np.float32)).cuda()
+          for _ in range(nb)]
+    for kind in (wf.WaveletKind.HAAR, wf.WaveletKind.DAUB4):
+        for path in ("auto", "ldg"):
+            os.environ["WF_D4_PATH"] = path
+            out = wf.fuse(pan, ms, wf.DwtReplace(kind))
+        os.environ.pop("WF_D4_PATH")
+        strips.fuse_scene_strips(kind, pan, ms)
+        wf.fuse(pan.double(), [m.double() for m in ms], wf.DwtReplace(kind))
+        if nb >= 2 and h >= 4:
+            for qp in ("scene", "generic"):
+                if qp == "generic":
+                    os.environ["WF_QNR_PATH"] = "generic"
+                wf.qnr(out, ms, pan)
+                os.environ.pop("WF_QNR_PATH", None)
+    if min(h, w) >= 4:
+        c = wf.dwt2d_forward(pan, wf.WaveletKind.DAUB4)
+        wf.dwt2d_inverse(c, wf.WaveletKind.DAUB4)
+    wf.resample_bilinear(ms[0], w, h)
+host = wf.fuse(np.ones((130, 264), np.float32), [np.ones((65, 132), np.float32)] * 3,
+               wf.DwtReplace(wf.WaveletKind.DAUB4))
+torch.cuda.synchronize()
+print("memcheck_small ok")
