@@ -9,6 +9,7 @@ to float64 (test_wavelet.py:219-222).
 from __future__ import annotations
 
 import atexit
+import contextlib
 import threading
 
 import numpy as np
@@ -16,8 +17,8 @@ import torch
 
 from . import _native
 
-_tls = threading.local()
 _ctxs: list[int] = []
+_free: list[int] = []
 _ctx_lock = threading.Lock()
 
 
@@ -64,19 +65,28 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def host_ctx() -> int:
-    """Per-thread wf_ctx for the host-buffer pipeline (re-entrant across
-    threads: each thread owns its streams and staging slots)."""
-    ctx = getattr(_tls, "ctx", None)
+@contextlib.contextmanager
+def host_ctx():
+    """Borrow a wf_ctx (streams + device slots + pinned staging) for one
+    host-buffer call. Contexts are pooled, not thread-local: concurrent
+    callers get distinct contexts (the library is re-entrant per context) and
+    later callers -- e.g. the fresh ThreadPoolExecutor threads of the
+    reference's fuse_tiled (tiling.py:185-189) -- reuse warm ones instead of
+    re-allocating pinned memory."""
+    with _ctx_lock:
+        ctx = _free.pop() if _free else None
     if ctx is None:
         dev = require_cuda()
         ctx = _native.load().wf_ctx_create(dev.index, 0)
         if not ctx:
             _native.check(5)
-        _tls.ctx = ctx
         with _ctx_lock:
             _ctxs.append(ctx)
-    return ctx
+    try:
+        yield ctx
+    finally:
+        with _ctx_lock:
+            _free.append(ctx)
 
 
 @atexit.register
@@ -91,3 +101,4 @@ def _release() -> None:
             except Exception:
                 pass
         _ctxs.clear()
+        _free.clear()

@@ -8,7 +8,12 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/wavefuse_b200.h"
@@ -140,19 +145,115 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
 }
 
 // ---------------------------------------------------------------------------
-// Host-buffer pipeline: rows are cut into strips; each strip's PAN rows, its
-// D4 halo rows and its MS rows go up, the strip kernel runs, the fused rows
-// come back. Three slots rotate over three streams so H2D of strip k+1, the
-// kernel of strip k and D2H of strip k-1 overlap (copy engines are
-// full-duplex on PCIe).
+// Host-buffer pipeline (wf_fuse_host_*): rows are cut into strips; each
+// strip's PAN rows, its D4 halo rows and its MS rows go up, the strip kernel
+// runs, the fused rows come back. Three slots rotate over three streams, so
+// the H2D of strip k+1, the kernel of strip k and the D2H of strip k-1
+// overlap (PCIe copy engines are full-duplex).
+//  * pinned caller buffers (cudaHostAlloc / cudaHostRegister / torch
+//    pin_memory): DMA straight from/to them;
+//  * pageable caller buffers (plain numpy): each slot owns a pinned staging
+//    buffer with the device slot's layout; the calling thread memcpy's strip
+//    k+3's inputs in and strip k's outputs out while the GPU works on the
+//    strips in between, so CPU copies, DMA and compute overlap and
+//    concurrent callers (one context each) scale instead of serialising on
+//    the driver's pageable-copy path.
 // ---------------------------------------------------------------------------
 constexpr int kSlots = 3;
 
+// Host-side copy workers for the pageable staging path: a strip's piece
+// copies are cut into ~2 MiB chunks that the caller and N persistent
+// workers drain together (first-touch page faults of fresh numpy outputs and
+// the copies themselves then use several cores instead of one).
+class CopyPool {
+ public:
+  struct Chunk {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void copy(const std::vector<Chunk>& pieces) {
+    std::vector<Chunk> work;
+    constexpr size_t kGrain = 2u << 20;
+    for (const Chunk& c : pieces)
+      for (size_t o = 0; o < c.bytes; o += kGrain)
+        work.push_back({static_cast<char*>(c.dst) + o, static_cast<const char*>(c.src) + o,
+                        c.bytes - o < kGrain ? c.bytes - o : kGrain});
+    if (th_.empty() || work.size() < 2) {
+      for (const Chunk& c : work) memcpy(c.dst, c.src, c.bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &work;
+      next_ = 0;
+      active_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain(work);
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [this] { return active_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void drain(const std::vector<Chunk>& w) {
+    for (size_t i = next_.fetch_add(1); i < w.size(); i = next_.fetch_add(1))
+      memcpy(w[i].dst, w[i].src, w[i].bytes);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::vector<Chunk>* job;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      drain(*job);
+      std::lock_guard<std::mutex> g(m_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::vector<Chunk>* job_ = nullptr;
+  std::atomic<size_t> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+int copy_threads() {
+  if (const char* e = getenv("WF_HOST_COPY_THREADS")) return atoi(e) > 0 ? atoi(e) : 0;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int n = hw >= 4 ? (int)(hw / 2) : 0;
+  return n > 8 ? 8 : n;
+}
+
 struct Slot {
   cudaStream_t stream = nullptr;
-  cudaEvent_t done = nullptr;
+  cudaEvent_t done = nullptr;  // the slot's last D2H has landed
   void* dbuf = nullptr;
   size_t bytes = 0;
+  void* hbuf = nullptr;  // pinned staging (pageable callers only)
+  size_t hbytes = 0;
+  int pend_r0 = -1, pend_rows = 0;  // strip whose outputs wait in hbuf
 };
 
 }  // namespace
@@ -161,9 +262,51 @@ struct wf_ctx {
   int device = 0;
   int strip_rows = 512;
   Slot slot[kSlots];
+  std::unique_ptr<CopyPool> pool;  // created on first pageable call
 };
 
 namespace {
+
+// Element offsets of one slot (identical for the device buffer and the pinned
+// staging buffer).
+struct SlotLayout {
+  size_t pan, top, bot, ms[wf::kMaxBandsPerLaunch * 64], mst[wf::kMaxBandsPerLaunch * 64],
+      out[wf::kMaxBandsPerLaunch * 64], total;
+};
+
+template <typename T>
+SlotLayout slot_layout(int S, int w, int nbands) {
+  auto up = [](size_t n) { return (n * sizeof(T) + 255) / 256 * 256 / sizeof(T); };
+  SlotLayout L{};
+  size_t o = 0;
+  L.pan = o;
+  o += up((size_t)S * w);
+  L.top = o;
+  o += up(2 * (size_t)w);
+  L.bot = o;
+  o += up(2 * (size_t)w);
+  for (int b = 0; b < nbands; ++b) {
+    L.ms[b] = o;
+    o += up((size_t)(S / 2) * (w / 2));
+    L.mst[b] = o;
+    o += up((size_t)(w / 2));
+  }
+  for (int b = 0; b < nbands; ++b) {
+    L.out[b] = o;
+    o += up((size_t)S * w);
+  }
+  L.total = o;
+  return L;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // plain pageable memory on some drivers reports an error
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
 
 template <typename T>
 int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const* out,
@@ -171,23 +314,24 @@ int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const*
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   if (int e = check_kind(kind)) return e;
   if (nbands < 1) return fail(WF_ERR_BAND_COUNT, "need at least one band");
+  if (nbands > (int)(sizeof(SlotLayout::ms) / sizeof(size_t)))
+    return fail(WF_ERR_BAND_COUNT, "too many bands (%d)", nbands);
+  if (!pan || !ms || !out) return fail(WF_ERR_VALUE, "null pointer argument");
   if ((h & 1) || (w & 1))
     return fail(WF_ERR_ODD_DIMENSION, "panchromatic plane %dx%d has an odd dimension", w, h);
   if (h < min_len(kind) || w < min_len(kind))
     return fail(WF_ERR_TOO_SMALL, "%dx%d below minimum %d per side", w, h, min_len(kind));
   if (cudaError_t e = cudaSetDevice(ctx->device)) return cuda_status(e, "cudaSetDevice");
 
+  bool pinned = is_pinned(pan);
+  for (int b = 0; b < nbands && pinned; ++b) pinned = is_pinned(ms[b]) && is_pinned(out[b]);
+
+  if (!pinned && !ctx->pool) ctx->pool.reset(new CopyPool(copy_threads()));
   int S = ctx->strip_rows;
   if (S > h) S = h;
   const int wh = w / 2;
-  // device slot layout: pan [S][w] | pan_top[2][w] | pan_bot[2][w] |
-  //                     ms [B][S/2][wh] | ms_top [B][wh] | out [B][S][w]
-  const size_t pan_e = (size_t)S * w, halo_e = 2 * (size_t)w;
-  const size_t ms_e = (size_t)(S / 2) * wh, mst_e = (size_t)wh, out_e = (size_t)S * w;
-  auto up16 = [](size_t n) { return (n * sizeof(T) + 255) / 256 * 256 / sizeof(T); };
-  const size_t need_e = up16(pan_e) + 2 * up16(halo_e) +
-                        (size_t)nbands * (up16(ms_e) + up16(mst_e) + up16(out_e));
-  const size_t need = need_e * sizeof(T);
+  const SlotLayout L = slot_layout<T>(S, w, nbands);
+  const size_t need = L.total * sizeof(T);
   for (int k = 0; k < kSlots; ++k) {
     Slot& sl = ctx->slot[k];
     if (sl.bytes < need) {
@@ -197,7 +341,30 @@ int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const*
       if (cudaError_t e = cudaMalloc(&sl.dbuf, need)) return cuda_status(e, "cudaMalloc slot");
       sl.bytes = need;
     }
+    if (!pinned && sl.hbytes < need) {
+      if (sl.hbuf) cudaFreeHost(sl.hbuf);
+      sl.hbuf = nullptr;
+      sl.hbytes = 0;
+      if (cudaError_t e = cudaHostAlloc(&sl.hbuf, need, cudaHostAllocPortable))
+        return cuda_status(e, "cudaHostAlloc staging");
+      sl.hbytes = need;
+    }
+    sl.pend_r0 = -1;
   }
+
+  // copy the finished outputs of a slot from its staging buffer to the caller
+  auto drain = [&](Slot& sl) -> int {
+    if (sl.pend_r0 < 0) return WF_OK;
+    if (cudaError_t e = cudaEventSynchronize(sl.done)) return cuda_status(e, "event sync");
+    const T* hb = static_cast<const T*>(sl.hbuf);
+    std::vector<CopyPool::Chunk> cp;
+    for (int b = 0; b < nbands; ++b)
+      cp.push_back({out[b] + (size_t)sl.pend_r0 * w, hb + L.out[b],
+                    sizeof(T) * (size_t)sl.pend_rows * w});
+    ctx->pool->copy(cp);
+    sl.pend_r0 = -1;
+    return WF_OK;
+  };
 
   std::vector<const T*> dms(nbands), dmst(nbands);
   std::vector<T*> dout(nbands);
@@ -206,55 +373,74 @@ int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const*
     const int rows = (h - r0) < S ? (h - r0) : S;
     Slot& sl = ctx->slot[k];
     cudaStream_t st = sl.stream;
-    T* base = static_cast<T*>(sl.dbuf);
-    T* dpan = base;
-    T* dtop = dpan + up16(pan_e);
-    T* dbot = dtop + up16(halo_e);
-    T* cur = dbot + up16(halo_e);
+    T* dbase = static_cast<T*>(sl.dbuf);
+    T* hbase = static_cast<T*>(sl.hbuf);
     for (int b = 0; b < nbands; ++b) {
-      T* dm = cur;
-      T* dmt = dm + up16(ms_e);
-      T* dot = dmt + up16(mst_e);
-      cur = dot + up16(out_e);
-      dms[b] = dm;
-      dmst[b] = dmt;
-      dout[b] = dot;
+      dms[b] = dbase + L.ms[b];
+      dmst[b] = dbase + L.mst[b];
+      dout[b] = dbase + L.out[b];
     }
-    // the slot's previous strip must have finished its D2H before reuse
-    // (same stream => already ordered)
-    cudaError_t e = cudaMemcpyAsync(dpan, pan + (size_t)r0 * w, sizeof(T) * (size_t)rows * w,
-                                    cudaMemcpyHostToDevice, st);
+    // input pieces: (slot offset, source, elements)
+    struct Piece {
+      size_t off;
+      const T* src;
+      size_t n;
+    };
+    std::vector<Piece> pieces;
+    pieces.push_back({L.pan, pan + (size_t)r0 * w, (size_t)rows * w});
     if (kind == WF_DAUB4) {
-      for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+      for (int q = 0; q < 2; ++q) {
         const int rt = (r0 - 2 + q + h) % h, rb = (r0 + rows + q) % h;
-        e = cudaMemcpyAsync(dtop + (size_t)q * w, pan + (size_t)rt * w, sizeof(T) * w,
-                            cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess)
-          e = cudaMemcpyAsync(dbot + (size_t)q * w, pan + (size_t)rb * w, sizeof(T) * w,
-                              cudaMemcpyHostToDevice, st);
+        pieces.push_back({L.top + (size_t)q * w, pan + (size_t)rt * w, (size_t)w});
+        pieces.push_back({L.bot + (size_t)q * w, pan + (size_t)rb * w, (size_t)w});
       }
     }
-    for (int b = 0; b < nbands && e == cudaSuccess; ++b) {
-      e = cudaMemcpyAsync(const_cast<T*>(dms[b]), ms[b] + (size_t)(r0 / 2) * wh,
-                          sizeof(T) * (size_t)(rows / 2) * wh, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess && kind == WF_DAUB4) {
+    for (int b = 0; b < nbands; ++b) {
+      pieces.push_back({L.ms[b], ms[b] + (size_t)(r0 / 2) * wh, (size_t)(rows / 2) * wh});
+      if (kind == WF_DAUB4) {
         const int mt = (r0 / 2 - 1 + h / 2) % (h / 2);
-        e = cudaMemcpyAsync(const_cast<T*>(dmst[b]), ms[b] + (size_t)mt * wh, sizeof(T) * wh,
-                            cudaMemcpyHostToDevice, st);
+        pieces.push_back({L.mst[b], ms[b] + (size_t)mt * wh, (size_t)wh});
       }
+    }
+    cudaError_t e = cudaSuccess;
+    if (pinned) {
+      for (const Piece& pc : pieces)
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(dbase + pc.off, pc.src, sizeof(T) * pc.n, cudaMemcpyHostToDevice,
+                              st);
+    } else {
+      // the slot's previous strip has fully completed once its outputs are
+      // drained (H2D -> kernel -> D2H are ordered on the slot's stream)
+      if (int rc = drain(sl)) return rc;
+      std::vector<CopyPool::Chunk> cp;
+      for (const Piece& pc : pieces) cp.push_back({hbase + pc.off, pc.src, sizeof(T) * pc.n});
+      ctx->pool->copy(cp);
+      for (const Piece& pc : pieces)
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(dbase + pc.off, hbase + pc.off, sizeof(T) * pc.n,
+                              cudaMemcpyHostToDevice, st);
     }
     if (e != cudaSuccess) return cuda_status(e, "H2D");
-    if (int rc = fuse_common<T>(kind, dpan, w, dtop, dbot, w, dms.data(), dmst.data(), wh,
-                                dout.data(), w, nbands, rows, w, true, st))
+    if (int rc = fuse_common<T>(kind, dbase + L.pan, w, dbase + L.top, dbase + L.bot, w,
+                                dms.data(), dmst.data(), wh, dout.data(), w, nbands, rows, w,
+                                true, st))
       return rc;
-    for (int b = 0; b < nbands && e == cudaSuccess; ++b)
-      e = cudaMemcpyAsync(out[b] + (size_t)r0 * w, dout[b], sizeof(T) * (size_t)rows * w,
-                          cudaMemcpyDeviceToHost, st);
+    for (int b = 0; b < nbands && e == cudaSuccess; ++b) {
+      T* dst = pinned ? out[b] + (size_t)r0 * w : hbase + L.out[b];
+      e = cudaMemcpyAsync(dst, dout[b], sizeof(T) * (size_t)rows * w, cudaMemcpyDeviceToHost, st);
+    }
     if (e != cudaSuccess) return cuda_status(e, "D2H");
+    if (!pinned) {
+      if ((e = cudaEventRecord(sl.done, st)) != cudaSuccess) return cuda_status(e, "event");
+      sl.pend_r0 = r0;
+      sl.pend_rows = rows;
+    }
   }
-  for (int q = 0; q < kSlots; ++q)
+  for (int q = 0; q < kSlots; ++q) {
+    if (int rc = drain(ctx->slot[q])) return rc;
     if (cudaError_t e = cudaStreamSynchronize(ctx->slot[q].stream))
       return cuda_status(e, "stream sync");
+  }
   return WF_OK;
 }
 
@@ -317,7 +503,10 @@ wf_ctx* wf_ctx_create(int device, int strip_rows) {
   if (strip_rows > 0) c->strip_rows = strip_rows & ~1;
   if (c->strip_rows < 2) c->strip_rows = 2;
   for (int k = 0; k < kSlots; ++k) {
-    if (cudaError_t e = cudaStreamCreateWithFlags(&c->slot[k].stream, cudaStreamNonBlocking)) {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->slot[k].stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+      e = cudaEventCreateWithFlags(&c->slot[k].done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
       cuda_status(e, "cudaStreamCreate");
       wf_ctx_destroy(c);
       return nullptr;
@@ -334,7 +523,9 @@ void wf_ctx_destroy(wf_ctx* c) {
       cudaStreamSynchronize(c->slot[k].stream);
       cudaStreamDestroy(c->slot[k].stream);
     }
+    if (c->slot[k].done) cudaEventDestroy(c->slot[k].done);
     if (c->slot[k].dbuf) cudaFree(c->slot[k].dbuf);
+    if (c->slot[k].hbuf) cudaFreeHost(c->slot[k].hbuf);
   }
   delete c;
 }

@@ -124,13 +124,12 @@ def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
     band_c = [np.ascontiguousarray(b, dtype=out_dt) for b in bands]
     outs = [np.empty((h, w), dtype=out_dt) for _ in bands]
     lib = _native.load()
-    ctx = _device.host_ctx()
     fn = lib.wf_fuse_host_f32 if out_dt == np.float32 else lib.wf_fuse_host_f64
     ms_ptrs = _native.ptr_array([b.ctypes.data for b in band_c])
     out_ptrs = _native.ptr_array([o.ctypes.data for o in outs])
-    torch.cuda.current_stream().synchronize()
-    _native.check(fn(ctx, KIND_CODE[kind], pan_c.ctypes.data, ms_ptrs, out_ptrs, len(bands),
-                     h, w))
+    with _device.host_ctx() as ctx:
+        _native.check(fn(ctx, KIND_CODE[kind], pan_c.ctypes.data, ms_ptrs, out_ptrs,
+                         len(bands), h, w))
     return outs
 
 

@@ -356,3 +356,31 @@ def test_strip_driver_single_rank_equals_fuse(kname):
     want = wf.fuse(pan, ms, wf.DwtReplace(KINDS[kname]))
     for a, b in zip(got, want):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("kname", list(KINDS))
+def test_host_pipeline_pinned_and_pageable(kname, pinned):
+    """wf_fuse_host_f32 through the C ABI: DMA straight from pinned buffers,
+    or through the context's pinned staging slots for pageable ones; several
+    strips (strip_rows=64 < H) so the 3-slot rotation and the D4 halo rows
+    at strip seams are exercised. Must equal the device-resident result."""
+    lib = _native.load()
+    H, W, B = 300, 264, 3
+    g = torch.Generator().manual_seed(21)
+    pan = torch.rand((H, W), generator=g) * 255
+    ms = [torch.rand((H // 2, W // 2), generator=g) * 255 for _ in range(B)]
+    out = [torch.empty((H, W)) for _ in range(B)]
+    if pinned:
+        pan, ms, out = pan.pin_memory(), [m.pin_memory() for m in ms], [o.pin_memory() for o in out]
+    ctx = lib.wf_ctx_create(0, 64)
+    try:
+        _native.check(lib.wf_fuse_host_f32(
+            ctx, 1 if kname == "haar" else 2, pan.data_ptr(),
+            _native.ptr_array([m.data_ptr() for m in ms]),
+            _native.ptr_array([o.data_ptr() for o in out]), B, H, W))
+    finally:
+        lib.wf_ctx_destroy(ctx)
+    want = wf.fuse(pan.cuda(), [m.cuda() for m in ms], wf.DwtReplace(KINDS[kname]))
+    for o, w_ in zip(out, want):
+        assert torch.equal(o, w_.cpu())

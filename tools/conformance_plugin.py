@@ -1,0 +1,82 @@
+"""pytest plugin: run the REFERENCE's own test suite against the B200 drop-in.
+
+    PYTHONPATH=baseline/_ref:. python -m pytest baseline/_ref/tests \
+        -p tools.conformance_plugin -q
+
+Before test collection it rebinds the reference's hot-path names (the binding
+sites listed in SURVEY.md 8(b)) to paper_1803_00737_b200, exactly as
+INTEGRATION.md section 1 tells a maintainer to: wavefuse.fusion.fuse_dwt
+(which routes fuse / fuse_tiled / the cluster worker / the CLI / the bench),
+the transforms, resample_bilinear, and the metrics. Kinds, exception classes
+and QualityReport are translated at the boundary. Nothing here computes: every
+rebinding calls the sm_100a library.
+"""
+
+from __future__ import annotations
+
+import functools
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1803_00737_b200 as wf  # noqa: E402
+from paper_1803_00737_b200 import errors as wf_errors  # noqa: E402
+
+ROUTED: dict[str, int] = {}
+
+
+def _install():
+    import wavefuse
+    import wavefuse.errors as ref_errors
+    import wavefuse.fusion as F
+    import wavefuse.metrics as M
+    import wavefuse.tiling as T
+    import wavefuse.wavelet as Wv
+
+    kinds = {Wv.WaveletKind.HAAR: wf.WaveletKind.HAAR, Wv.WaveletKind.DAUB4: wf.WaveletKind.DAUB4}
+
+    def translate(fn, name):
+        @functools.wraps(fn)
+        def call(*args, **kwargs):
+            ROUTED[name] = ROUTED.get(name, 0) + 1
+            args = [kinds.get(a, a) if isinstance(a, Wv.WaveletKind) else a for a in args]
+            try:
+                out = fn(*args, **kwargs)
+            except wf_errors.FusionError as e:
+                raise getattr(ref_errors, type(e).__name__)(str(e)) from None
+            if isinstance(out, wf.QualityReport):
+                out = M.QualityReport(ergas=out.ergas, q_per_band=out.q_per_band,
+                                      d_lambda=out.d_lambda, d_s=out.d_s, qnr=out.qnr)
+            return out
+        return call
+
+    fuse_dwt = translate(wf.fuse_dwt, "fuse_dwt")
+    fwd2, inv2 = translate(wf.dwt2d_forward, "dwt2d_forward"), translate(wf.dwt2d_inverse, "dwt2d_inverse")
+    fwd1, inv1 = translate(wf.dwt1d_forward, "dwt1d_forward"), translate(wf.dwt1d_inverse, "dwt1d_inverse")
+    resample = translate(wf.resample_bilinear, "resample_bilinear")
+    F.fuse_dwt = fuse_dwt
+    F.dwt2d_forward, F.dwt2d_inverse = fwd2, inv2
+    F.resample_bilinear = resample
+    T.resample_bilinear = resample
+    Wv.dwt1d_forward, Wv.dwt1d_inverse = fwd1, inv1
+    Wv.dwt2d_forward, Wv.dwt2d_inverse = fwd2, inv2
+    M.resample_bilinear = resample
+    for name in ("degrade", "q_index", "ergas", "d_lambda", "d_s", "qnr"):
+        setattr(M, name, translate(getattr(wf, name), name))
+    for name in ("fuse_dwt", "resample_bilinear", "dwt1d_forward", "dwt1d_inverse",
+                 "dwt2d_forward", "dwt2d_inverse", "degrade", "q_index", "ergas", "d_lambda",
+                 "d_s", "qnr"):
+        if hasattr(wavefuse, name):
+            setattr(wavefuse, name, getattr(F, name, None) or getattr(Wv, name, None)
+                    or getattr(M, name))
+
+
+def pytest_configure(config):
+    _install()
+
+
+def pytest_terminal_summary(terminalreporter):
+    terminalreporter.write_line("B200 drop-in calls routed: " +
+                                ", ".join(f"{k}={v}" for k, v in sorted(ROUTED.items())))
