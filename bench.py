@@ -283,6 +283,63 @@ def measure_e2e(scene, kind, steps, dist):
     return sec, h2d, d2h, ok
 
 
+def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
+    """the same scene in the paper's 8 bpp transfer
+    representation (uint8 in, quantised uint8 out, float32 arithmetic). A
+    step = one launch of the 8 bpp kernel over the whole scene; algorithmic
+    bytes (1 + 1.25 B) per PAN px."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind, _native
+    from paper_1803_00737_b200.fusion import _quantize_dev
+    from paper_1803_00737_b200.wavelet import KIND_CODE
+
+    lib = _native.load()
+    h, w = scene.shape
+    pan = _quantize_dev(scene.pan)
+    ms = [_quantize_dev(m) for m in scene.ms]
+    out = [torch.empty((h, w), dtype=torch.uint8, device=pan.device) for _ in ms]
+    ms_p = _native.ptr_array([m.data_ptr() for m in ms])
+    out_p = _native.ptr_array([o.data_ptr() for o in out])
+    nbytes = h * w + len(ms) * ((h // 2) * (w // 2) + h * w)
+    res = {}
+    for kind in (WaveletKind.HAAR, WaveletKind.DAUB4):
+        code = KIND_CODE[kind]
+        stream = torch.cuda.current_stream()
+        sp = stream.cuda_stream
+
+        def run():
+            _native.check(lib.wf_fuse_bands_u8(code, pan.data_ptr(), w, ms_p, w // 2, out_p, w,
+                                               len(ms), h, w, sp))
+
+        for _ in range(warmup):
+            run()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_t = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms_t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_t = float(t.item())
+        per = ms_t / steps
+        achieved = nbytes / (per * 1e-3) / 1e9
+        res[kind.value] = {
+            "value": round(world * h * w / (per * 1e-3) / 1e6, 3),
+            "ms_per_step": round(per, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_launch": nbytes},
+        }
+    return {"unit": UNIT, "dtype": "u8 in/out, f32 arithmetic", **res}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -333,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
                 "matches_device_result": ok,
             },
         }
+    u8 = measure_u8(scene, args.steps, args.warmup, dist, world, local_rank, peak)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -379,6 +437,7 @@ def run_ours(args, rank, world, local_rank):
                 "e2e": results["daub4"]["e2e"],
                 "cpu_baseline": cpu.get("daub4"),
             },
+            "u8_8bpp": u8,
         }
         print(json.dumps(line), flush=True)
     if dist:

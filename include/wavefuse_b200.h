@@ -116,6 +116,28 @@ int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const
 int wf_fuse_host_f64(wf_ctx* ctx, int kind, const double* pan, const double* const* ms,
                      double* const* out, int nbands, int h, int w);
 
+/* ---- 8 bpp transfer representation (tiling.py:163-172) ---
+ * uint8 PAN/MS in, float32 arithmetic, quantised uint8 out: the fused
+ * equivalent of [quantize(p) for p in fuse_tile_quantized(pan, ms, method)]
+ * (tiling.py:268-269, imageio.py:115-123). Haar is bit-identical to the
+ * reference (all intermediates are multiples of 1/4); D4 may differ by one
+ * LSB where the float64 value lies within ~1e-4 of a .5 rounding boundary.
+ * Haar needs W % 16 == 0, D4 W % 32 == 0, rows 16-byte aligned. */
+int wf_fuse_bands_u8(int kind, const uint8_t* pan, int64_t pan_pitch, const uint8_t* const* ms,
+                     int64_t ms_pitch, uint8_t* const* out, int64_t out_pitch, int nbands, int h,
+                     int w, void* stream);
+int wf_fuse_strip_u8(int kind, const uint8_t* pan, int64_t pan_pitch, const uint8_t* pan_top,
+                     const uint8_t* pan_bot, int64_t halo_pitch, const uint8_t* const* ms,
+                     const uint8_t* const* ms_top, int64_t ms_pitch, uint8_t* const* out,
+                     int64_t out_pitch, int nbands, int rows, int w, void* stream);
+int wf_fuse_host_u8(wf_ctx* ctx, int kind, const uint8_t* pan, const uint8_t* const* ms,
+                    uint8_t* const* out, int nbands, int h, int w);
+/* imageio.py:104-113 to_plane (uint8 -> float32) and :115-123 quantize. */
+int wf_u8_to_f32(const uint8_t* in, int64_t in_pitch, int h, int w, float* out,
+                 int64_t out_pitch, void* stream);
+int wf_quantize_f32(const float* in, int64_t in_pitch, int h, int w, uint8_t* out,
+                    int64_t out_pitch, void* stream);
+
 /* ---- standalone transforms --------------------------------------------- */
 int wf_dwt2d_forward_f32(int kind, const float* in, int64_t in_pitch, float* out,
                          int64_t out_pitch, int h, int w, void* stream);

@@ -243,3 +243,25 @@ def fuse_parallel(pan, bands, kind, threads: int | None = None,
     with ThreadPoolExecutor(max_workers=threads) as ex:
         list(ex.map(work, starts))
     return outs
+
+
+# ---------------------------------------------------------------------------
+# 8 bpp transfer representation
+# ---------------------------------------------------------------------------
+def quantize(plane) -> np.ndarray:
+    """imageio.py:115-123: clamp to [0, 255], then floor(x + 0.5) (half away
+    from zero for the clamped, non-negative values), in the plane's dtype."""
+    p = np.asarray(plane)
+    c = np.minimum(np.maximum(p, p.dtype.type(0.0)), p.dtype.type(255.0))
+    return np.floor(c + p.dtype.type(0.5)).astype(np.uint8)
+
+
+def fuse_tile_quantized(pan_u8, ms_u8, kind) -> list[np.ndarray]:
+    """tiling.py:163-172: uint8 tile -> float32 planes -> fuse."""
+    return fuse(np.asarray(pan_u8).astype(np.float32),
+                [np.asarray(b).astype(np.float32) for b in ms_u8], kind)
+
+
+def fuse_quantized(pan_u8, ms_u8, kind) -> list[np.ndarray]:
+    """tiling.py:268-269: what a worker returns for one 8 bpp tile."""
+    return [quantize(p) for p in fuse_tile_quantized(pan_u8, ms_u8, kind)]

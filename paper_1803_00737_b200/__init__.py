@@ -21,7 +21,17 @@ from .errors import (
     TooSmall,
     ZeroBandMean,
 )
-from .fusion import DwtReplace, FusionMethod, fuse, fuse_dwt, method_from_name, resample_bilinear
+from .fusion import (
+    DwtReplace,
+    FusionMethod,
+    fuse,
+    fuse_dwt,
+    fuse_quantized,
+    fuse_tile_quantized,
+    method_from_name,
+    quantize,
+    resample_bilinear,
+)
 from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, q_index, qnr
 from .wavelet import (
     FilterBank,
@@ -64,8 +74,11 @@ __all__ = [
     "ergas",
     "fuse",
     "fuse_dwt",
+    "fuse_quantized",
+    "fuse_tile_quantized",
     "method_from_name",
     "q_index",
     "qnr",
+    "quantize",
     "resample_bilinear",
 ]

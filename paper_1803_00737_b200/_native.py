@@ -62,6 +62,11 @@ def _declare(lib: ctypes.CDLL) -> None:
         sig[f"wf_resample_bilinear_{t}"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_int, c_int,
                                             c_vp]
     sig["wf_synth_plane_f32"] = [c_vp, c_i64, c_int, c_int, c_u64, c_u32, c_int, c_int, c_vp]
+    sig["wf_fuse_bands_u8"] = sig["wf_fuse_bands_f32"]
+    sig["wf_fuse_strip_u8"] = sig["wf_fuse_strip_f32"]
+    sig["wf_fuse_host_u8"] = sig["wf_fuse_host_f32"]
+    sig["wf_u8_to_f32"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp]
+    sig["wf_quantize_f32"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp]
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args

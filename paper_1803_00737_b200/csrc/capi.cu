@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/wavefuse_b200.h"
@@ -89,7 +90,9 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
 
   const int vw = 16 / (int)sizeof(T);  // elements per 16 B
   bool vec = al16(pan) && pan_pitch % vw == 0 && out_pitch % vw == 0 && ms_pitch % 2 == 0;
-  if (kind == WF_HAAR) vec = vec && (w % 4 == 0);
+  if (kind == WF_HAAR) vec = vec && (w % (sizeof(T) == 1 ? 16 : 4) == 0);
+  // bulk-copy halo pieces are 16 bytes: 4 elements (f32/f64 use >= 4), 16 for u8
+  const int halo = 16 / (int)sizeof(T) >= 4 ? 16 / (int)sizeof(T) : 4;
   for (int b = 0; b < nbands; ++b) {
     if (!ms[b] || !out[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
     vec = vec && al16(out[b]) && al16(ms[b]);
@@ -134,10 +137,16 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
         a.ms_top[b] = strip ? ms_top[b0 + b]
                             : ms[b0 + b] + (int64_t)(rows / 2 - 1) * ms_pitch;
     }
-    bool tma = allow_tma && kind == WF_DAUB4 && vec && w % 8 == 0 && row16(pan_pitch) &&
-               row16(ms_pitch) && row16(a.halo_pitch) && al16(a.pan_top) && al16(a.pan_bot);
+    bool tma = (allow_tma || sizeof(T) == 1) && kind == WF_DAUB4 && vec && w % (2 * halo) == 0 &&
+               row16(pan_pitch) && row16(ms_pitch) && row16(a.halo_pitch) && al16(a.pan_top) &&
+               al16(a.pan_bot);
     for (int b = 0; b < nb && tma; ++b) tma = al16(a.ms_top[b]);
-    cudaError_t e = wf::launch_fuse<T, T>(kind, a, vec, tma, s, tune);
+    if (sizeof(T) == 1 && !(kind == WF_DAUB4 ? tma : vec))
+      return fail(WF_ERR_VALUE,
+                  "8 bpp kernels need W %% %d == 0 and 16-byte aligned rows (got W=%d)",
+                  kind == WF_DAUB4 ? 2 * halo : 16, w);
+    using Acc = typename std::conditional<sizeof(T) == 1, float, T>::type;
+    cudaError_t e = wf::launch_fuse<T, Acc>(kind, a, vec, tma, s, tune);
     if (e != cudaSuccess) return cuda_status(e, "fuse launch");
     ++g_launches;
   }
@@ -537,6 +546,43 @@ int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const
 int wf_fuse_host_f64(wf_ctx* ctx, int kind, const double* pan, const double* const* ms,
                      double* const* out, int nbands, int h, int w) {
   return fuse_host<double>(ctx, kind, pan, ms, out, nbands, h, w);
+}
+
+int wf_fuse_bands_u8(int kind, const uint8_t* pan, int64_t pan_pitch, const uint8_t* const* ms,
+                     int64_t ms_pitch, uint8_t* const* out, int64_t out_pitch, int nbands, int h,
+                     int w, void* stream) {
+  return fuse_common<uint8_t>(kind, pan, pan_pitch, nullptr, nullptr, 0, ms, nullptr, ms_pitch,
+                              out, out_pitch, nbands, h, w, false, (cudaStream_t)stream);
+}
+int wf_fuse_strip_u8(int kind, const uint8_t* pan, int64_t pan_pitch, const uint8_t* pan_top,
+                     const uint8_t* pan_bot, int64_t halo_pitch, const uint8_t* const* ms,
+                     const uint8_t* const* ms_top, int64_t ms_pitch, uint8_t* const* out,
+                     int64_t out_pitch, int nbands, int rows, int w, void* stream) {
+  return fuse_common<uint8_t>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
+                              ms_pitch, out, out_pitch, nbands, rows, w, true,
+                              (cudaStream_t)stream);
+}
+int wf_fuse_host_u8(wf_ctx* ctx, int kind, const uint8_t* pan, const uint8_t* const* ms,
+                    uint8_t* const* out, int nbands, int h, int w) {
+  return fuse_host<uint8_t>(ctx, kind, pan, ms, out, nbands, h, w);
+}
+
+int wf_u8_to_f32(const uint8_t* in, int64_t in_pitch, int h, int w, float* out,
+                 int64_t out_pitch, void* stream) {
+  if (!in || !out || h < 0 || w < 0) return fail(WF_ERR_VALUE, "bad conversion arguments");
+  if (h == 0 || w == 0) return WF_OK;
+  cudaError_t e = wf::launch_u8_to_f32(in, in_pitch, h, w, out, out_pitch, (cudaStream_t)stream);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e, "wf_u8_to_f32");
+}
+
+int wf_quantize_f32(const float* in, int64_t in_pitch, int h, int w, uint8_t* out,
+                    int64_t out_pitch, void* stream) {
+  if (!in || !out || h < 0 || w < 0) return fail(WF_ERR_VALUE, "bad quantize arguments");
+  if (h == 0 || w == 0) return WF_OK;
+  cudaError_t e = wf::launch_quantize(in, in_pitch, h, w, out, out_pitch, (cudaStream_t)stream);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e, "wf_quantize_f32");
 }
 
 #define WF_DWT2D(NAME, T, INV)                                                               \

@@ -386,6 +386,118 @@ cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, bool tma, cuda
   }
 }
 
+// ---------------------------------------------------------------------------
+// 8 bpp Haar (the paper's transfer representation, tiling.py:163-172): uint8
+// PAN/MS in, quantised uint8 out (imageio.py:115-123 fused into the store).
+// With integer inputs every intermediate is a multiple of 1/4, exact in
+// float32, so the result is bit-identical to quantize(fuse_dwt(...)) of the
+// float64 reference. A thread owns 16 PAN columns x 2 rows (uint4 I/O).
+// ---------------------------------------------------------------------------
+template <int NB>
+__global__ void __launch_bounds__(kHaarThreads)
+    fuse_haar_u8_kernel(const FuseArgs<uint8_t> a) {
+  const int g = blockIdx.x * kHaarThreads + threadIdx.x;  // 16-column group
+  const int c = 16 * g;
+  if (c >= a.W) return;
+  const int npairs = a.rows >> 1;
+  const int i_begin = blockIdx.y * kHaarPairsPerThread;
+#pragma unroll
+  for (int s = 0; s < kHaarPairsPerThread; ++s) {
+    const int i = i_begin + s;
+    if (i >= npairs) break;
+    const uint8_t* r0 = a.pan + (long long)(2 * i) * a.pan_pitch + c;
+    uint4 w0, w1;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(w0.x), "=r"(w0.y), "=r"(w0.z), "=r"(w0.w)
+        : "l"(r0));
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(w1.x), "=r"(w1.y), "=r"(w1.z), "=r"(w1.w)
+        : "l"(r0 + a.pan_pitch));
+    // Integer form of the same arithmetic: every value is a multiple of 1/4,
+    // so with P = 4*pan, C = 2 - (sum of the 2x2 cell) and M = 4*ms,
+    //   quantize(pan + ms - mean2x2) = clamp((P + M + C) >> 2, 0, 255)
+    // (arithmetic shift = floor; identical to floor(clamp(v) + 0.5) of
+    // imageio.py:115-123 on the exact float value).
+    const uint32_t p0w[4] = {w0.x, w0.y, w0.z, w0.w}, p1w[4] = {w1.x, w1.y, w1.z, w1.w};
+    int q0[16], q1[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      q0[k] = (int)((p0w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+      q1[k] = (int)((p1w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    }
+    int cell[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cell[k] = 2 - (q0[2 * k] + q0[2 * k + 1] + q1[2 * k] + q1[2 * k + 1]);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      q0[k] *= 4;
+      q1[k] *= 4;
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      uint2 mw;
+      asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+          : "=r"(mw.x), "=r"(mw.y)
+          : "l"(a.ms[b] + (long long)i * a.ms_pitch + (c >> 1)));
+      const uint32_t mwv[2] = {mw.x, mw.y};
+      uint32_t r0v[16], r1v[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = 4 * (int)((mwv[k >> 2] >> (8 * (k & 3))) & 0xffu) + cell[k];
+#pragma unroll
+        for (int x = 2 * k; x < 2 * k + 2; ++x) {
+          r0v[x] = (uint32_t)min(max((q0[x] + t) >> 2, 0), 255);
+          r1v[x] = (uint32_t)min(max((q1[x] + t) >> 2, 0), 255);
+        }
+      }
+      uint32_t o0[4], o1[4];
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd) {
+        o0[wd] = __byte_perm(__byte_perm(r0v[4 * wd], r0v[4 * wd + 1], 0x0040),
+                             __byte_perm(r0v[4 * wd + 2], r0v[4 * wd + 3], 0x0040), 0x5410);
+        o1[wd] = __byte_perm(__byte_perm(r1v[4 * wd], r1v[4 * wd + 1], 0x0040),
+                             __byte_perm(r1v[4 * wd + 2], r1v[4 * wd + 3], 0x0040), 0x5410);
+      }
+      uint8_t* w = a.out[b] + (long long)(2 * i) * a.out_pitch + c;
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(w), "r"(o0[0]), "r"(o0[1]),
+                   "r"(o0[2]), "r"(o0[3])
+                   : "memory");
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(w + a.out_pitch),
+                   "r"(o1[0]), "r"(o1[1]), "r"(o1[2]), "r"(o1[3])
+                   : "memory");
+    }
+  }
+}
+
+template <int NB>
+static cudaError_t launch_haar_u8(const FuseArgs<uint8_t>& a, cudaStream_t s) {
+  const int ng = (a.W + 15) / 16;
+  dim3 grid((ng + kHaarThreads - 1) / kHaarThreads,
+            ((a.rows >> 1) + kHaarPairsPerThread - 1) / kHaarPairsPerThread);
+  fuse_haar_u8_kernel<NB><<<grid, kHaarThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// uint8 specialisation: Haar needs 16-byte rows (vec), D4 the bulk-copy
+// geometry (tma); the caller checks both before launching.
+template <>
+cudaError_t launch_fuse<uint8_t, float>(int kind, const FuseArgs<uint8_t>& a, bool vec, bool tma,
+                                        cudaStream_t s, const LaunchTuning& tune) {
+  if (kind == kDaub4) return tma ? launch_fuse_d4_tma<uint8_t>(a, s, tune) : cudaErrorInvalidValue;
+  if (!vec) return cudaErrorInvalidValue;
+  switch (a.nbands) {
+    case 1: return launch_haar_u8<1>(a, s);
+    case 2: return launch_haar_u8<2>(a, s);
+    case 3: return launch_haar_u8<3>(a, s);
+    case 4: return launch_haar_u8<4>(a, s);
+    case 5: return launch_haar_u8<5>(a, s);
+    case 6: return launch_haar_u8<6>(a, s);
+    case 7: return launch_haar_u8<7>(a, s);
+    case 8: return launch_haar_u8<8>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template cudaError_t launch_fuse<float, float>(int, const FuseArgs<float>&, bool, bool,
                                                cudaStream_t, const LaunchTuning&);
 template cudaError_t launch_fuse<double, double>(int, const FuseArgs<double>&, bool, bool,

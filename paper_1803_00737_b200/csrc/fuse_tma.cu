@@ -16,6 +16,12 @@
 //    no lane-0/lane-31 special cases -- release the slot (empty barrier) and
 //    stream the fused rows of every band to HBM with st.global.cs.
 //
+// Element types: float / double (the reference's dtype rule) and uint8 --
+// the paper's 8 bpp transfer representation (tiling.py:163-172):
+// uint8 PAN/MS in, float32 arithmetic, and the reference's quantize
+// (imageio.py:115-123: clamp to [0, 255], floor(x + 0.5) in float32) fused
+// into the store, so 8 bpp tiles move 1 + 1.25 B per PAN px per band.
+//
 // Bytes in flight live in shared memory, not in registers, so a handful of
 // warps per SM keep >100 KB of HBM reads outstanding.
 #include "wf_common.cuh"
@@ -23,6 +29,17 @@
 #include "wf_tma.cuh"
 
 namespace wf {
+
+template <typename T>
+struct TmaTraits {
+  using Acc = T;
+  static constexpr int HALO = 16 / (int)sizeof(T) >= 4 ? 16 / (int)sizeof(T) : 4;
+};
+template <>
+struct TmaTraits<uint8_t> {
+  using Acc = float;
+  static constexpr int HALO = 16;  // bulk-copy pieces are multiples of 16 bytes
+};
 
 template <typename Acc>
 __device__ __forceinline__ Acc dot4t(Acc h0, Acc h1, Acc h2, Acc h3, Acc x0, Acc x1, Acc x2,
@@ -44,30 +61,55 @@ struct TmaRows {
   }
 };
 
-template <typename T>
-__device__ __forceinline__ void lds2(const T* p, T& x, T& y) {
+// two consecutive shared-memory elements as Acc
+template <typename T, typename Acc>
+__device__ __forceinline__ void lds2(const T* p, Acc& x, Acc& y) {
   if constexpr (sizeof(T) == 4) {
     const float2 v = *reinterpret_cast<const float2*>(p);
     x = v.x;
     y = v.y;
-  } else {
+  } else if constexpr (sizeof(T) == 8) {
     const double2 v = *reinterpret_cast<const double2*>(p);
     x = v.x;
     y = v.y;
+  } else {
+    x = (Acc)p[0];
+    y = (Acc)p[1];
+  }
+}
+
+// imageio.py:115-123 quantize (clamp to [0, 255], then floor(x + 0.5) in
+// float32). For |x| < 2^22, x + 0.5 is exact, so clamping after the floor is
+// the same function: FADD, F2I.U32 with round-down (saturates negatives to
+// 0), IMNMX.
+__device__ __forceinline__ uint32_t quantize_u8(float v) {
+  return min(__float2uint_rd(__fadd_rn(v, 0.5f)), 255u);
+}
+
+template <typename T, typename Acc>
+__device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
+  if constexpr (sizeof(T) == 1) {
+    const uint32_t lo = __byte_perm(quantize_u8(o[0]), quantize_u8(o[1]), 0x0040);
+    const uint32_t hi = __byte_perm(quantize_u8(o[2]), quantize_u8(o[3]), 0x0040);
+    const uint32_t v = __byte_perm(lo, hi, 0x5410);
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    store4_vec<Acc>(p, o);
   }
 }
 
 template <typename T, int NB, int NCW>
 __global__ void __launch_bounds__(32 * (NCW + 1))
     fuse_d4_tma_kernel(const FuseArgs<T> a, int S) {
-  using Acc = T;
+  using Acc = typename TmaTraits<T>::Acc;
+  constexpr int HALO = TmaTraits<T>::HALO;
   constexpr int CW = 128 * NCW;
-  constexpr int PROW = CW + 8;     // [4 left halo | CW | 4 right halo]
-  constexpr int MROW = CW / 2 + 4;  // [4 left halo | CW/2]
+  constexpr int PROW = CW + 2 * HALO;  // [HALO left | CW | HALO right]
+  constexpr int MROW = CW / 2 + HALO;  // [HALO left | CW/2]
   constexpr int SLOT = 2 * PROW + NB * MROW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* slots = reinterpret_cast<T*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * SLOT * sizeof(T));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)S * SLOT * sizeof(T) + 15) & ~size_t(15)));
   uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -93,13 +135,13 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
   if (warp == NCW) {
     // ------------------------------ producer ------------------------------
     const TmaRows<T> pan{a.pan, a.pan_top, a.pan_bot, a.pan_pitch, a.halo_pitch, a.rows};
-    const uint32_t pan_row_bytes = (uint32_t)((len + 8) * sizeof(T));
-    const uint32_t ms_row_bytes = (uint32_t)((len / 2 + 4) * sizeof(T));
+    const uint32_t pan_row_bytes = (uint32_t)((len + 2 * HALO) * sizeof(T));
+    const uint32_t ms_row_bytes = (uint32_t)((len / 2 + HALO) * sizeof(T));
     // per-lane copy role (fixed for the whole task)
     const int q = lane / 3, piece = lane % 3;  // lanes 0..5: PAN row q, piece
     const int mb = (lane - 6) >> 1, mpiece = (lane - 6) & 1;  // lanes 6..: MS band, piece
-    const int lcol = wrap(base - 4, W), rcol = (base + len) % W;
-    const int mlcol = wrap((base >> 1) - 4, Wh);
+    const int lcol = wrap(base - HALO, W), rcol = (base + len) % W;
+    const int mlcol = wrap((base >> 1) - HALO, Wh);
     for (int n = 0; n < nloads; ++n) {
       const int s = n % S, r = n / S;
       if (r > 0 && lane == 0) tma::mbar_wait(&empty[s], (r - 1) & 1);
@@ -115,19 +157,31 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
         const T* row = pan.row(2 * (i0 + k) + 2 + q);
         T* dst = slot + q * PROW;
         if (piece == 0)
-          tma::bulk_g2s(dst, row + lcol, 4 * sizeof(T), &full[s]);
+          tma::bulk_g2s(dst, row + lcol, HALO * sizeof(T), &full[s]);
         else if (piece == 1)
-          tma::bulk_g2s(dst + 4, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
+          tma::bulk_g2s(dst + HALO, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
         else
-          tma::bulk_g2s(dst + 4 + len, row + rcol, 4 * sizeof(T), &full[s]);
+          tma::bulk_g2s(dst + HALO + len, row + rcol, HALO * sizeof(T), &full[s]);
       } else if (with_ms && lane < 6 + 2 * NB) {
         const int mrow = i0 + k;
-        const T* mr = mrow < 0 ? a.ms_top[mb] : a.ms[mb] + (long long)mrow * a.ms_pitch;
+        const T* mr = a.ms[0];
+#pragma unroll
+        for (int b = 1; b < NB; ++b)  // static indexing keeps the band table in the param bank
+          if (mb == b) mr = a.ms[b];
+        if (mrow < 0) {
+          mr = a.ms_top[0];
+#pragma unroll
+          for (int b = 1; b < NB; ++b)
+            if (mb == b) mr = a.ms_top[b];
+        } else {
+          mr += (long long)mrow * a.ms_pitch;
+        }
         T* dst = slot + 2 * PROW + mb * MROW;
         if (mpiece == 0)
-          tma::bulk_g2s(dst, mr + mlcol, 4 * sizeof(T), &full[s]);
+          tma::bulk_g2s(dst, mr + mlcol, HALO * sizeof(T), &full[s]);
         else
-          tma::bulk_g2s(dst + 4, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)), &full[s]);
+          tma::bulk_g2s(dst + HALO, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)),
+                        &full[s]);
       }
     }
     return;
@@ -152,19 +206,19 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
     Acc v[2][8];  // PAN cols c-2 .. c+5 of the slot's two rows
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const T* pr = slot + q * PROW + 4 + rel;
-      lds2(pr - 2, v[q][0], v[q][1]);
-      lds2(pr, v[q][2], v[q][3]);
-      lds2(pr + 2, v[q][4], v[q][5]);
-      lds2(pr + 4, v[q][6], v[q][7]);
+      const T* pr = slot + q * PROW + HALO + rel;
+      lds2<T, Acc>(pr - 2, v[q][0], v[q][1]);
+      lds2<T, Acc>(pr, v[q][2], v[q][3]);
+      lds2<T, Acc>(pr + 2, v[q][4], v[q][5]);
+      lds2<T, Acc>(pr + 4, v[q][6], v[q][7]);
     }
     Acc m[NB][3];
     if (n >= 1) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        const T* mr = slot + 2 * PROW + b * MROW + 4 + (rel >> 1);
-        m[b][0] = mr[-1];
-        lds2(mr, m[b][1], m[b][2]);
+        const T* mr = slot + 2 * PROW + b * MROW + HALO + (rel >> 1);
+        m[b][0] = (Acc)mr[-1];
+        lds2<T, Acc>(mr, m[b][1], m[b][2]);
       }
     }
     __syncwarp();
@@ -207,7 +261,11 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
               o[1] = pa[p][1] + fma(h1, v0, h3 * vm);
               o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
               o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
-              store4_vec<Acc>(a.out[b] + (long long)(2 * i + p) * a.out_pitch + c, o);
+              T* orow = a.out[0];
+#pragma unroll
+              for (int bb = 1; bb < NB; ++bb)
+                if (b == bb) orow = a.out[bb];
+              store4_out<T, Acc>(orow + (long long)(2 * i + p) * a.out_pitch + c, o);
             }
           }
 #pragma unroll
@@ -229,8 +287,9 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
 template <typename T, int NB, int NCW>
 static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const LaunchTuning& tune) {
   FuseArgs<T> a = a0;
+  constexpr int HALO = TmaTraits<T>::HALO;
   constexpr int CW = 128 * NCW;
-  constexpr int SLOT = 2 * (CW + 8) + NB * (CW / 2 + 4);
+  constexpr int SLOT = 2 * (CW + 2 * HALO) + NB * (CW / 2 + HALO);
   const int npairs = a.rows >> 1;
   int S = tune.d4_stages > 0 ? tune.d4_stages : 0;
   if (S <= 0) {
@@ -239,13 +298,18 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
     if (S < 2) S = 2;
     if (S > 8) S = 8;
   }
-  const size_t smem = (size_t)S * SLOT * sizeof(T) + 2 * S * sizeof(uint64_t);
+  const size_t smem =
+      (((size_t)S * SLOT * sizeof(T) + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t);
   auto kern = fuse_d4_tma_kernel<T, NB, NCW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   a.n_colbands = (a.W + CW - 1) / CW;
-  int P = tune.d4_pairs > 0 ? tune.d4_pairs : 8;  // measured best on Landsat (tools/sweep_d4.py)
+  // row pairs per CTA: 8 measured best for multi-band f32 on Landsat, longer
+  // runs amortise the 2-pair prologue when there is little per-pair work
+  // (tools/sweep_d4.py on the Landsat scene: B >= 4 -> 4, B = 2..3 -> 8, B = 1 -> 32)
+  int P = tune.d4_pairs > 0 ? tune.d4_pairs
+                            : (sizeof(T) == 1 ? 16 : (NB == 1 ? 32 : (NB <= 3 ? 8 : 4)));
   if (P > npairs) P = npairs;
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;
@@ -273,5 +337,7 @@ template cudaError_t launch_fuse_d4_tma<float>(const FuseArgs<float>&, cudaStrea
                                                const LaunchTuning&);
 template cudaError_t launch_fuse_d4_tma<double>(const FuseArgs<double>&, cudaStream_t,
                                                 const LaunchTuning&);
+template cudaError_t launch_fuse_d4_tma<uint8_t>(const FuseArgs<uint8_t>&, cudaStream_t,
+                                                 const LaunchTuning&);
 
 }  // namespace wf

@@ -197,7 +197,41 @@ __global__ void synth_kernel(float* __restrict__ out, long long pitch, int rows,
   }
 }
 
+// ---- 8 bpp conversions (imageio.py:104-123) --------------------------------
+__global__ void u8_to_f32_kernel(const uint8_t* __restrict__ in, long long ip, int h, int w,
+                                 float* __restrict__ out, long long op) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+    if (x < w) out[(long long)y * op + x] = (float)in[(long long)y * ip + x];
+}
+
+// quantize: clamp to [0, 255] then floor(x + 0.5), in float32 like numpy on a
+// float32 plane (imageio.py:115-123)
+__global__ void quantize_kernel(const float* __restrict__ in, long long ip, int h, int w,
+                                uint8_t* __restrict__ out, long long op) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+    if (x < w) {
+      const float v = fminf(fmaxf(in[(long long)y * ip + x], 0.0f), 255.0f);
+      out[(long long)y * op + x] = (uint8_t)floorf(__fadd_rn(v, 0.5f));
+    }
+}
+
 // ---- launchers --------------------------------------------------------------
+cudaError_t launch_u8_to_f32(const uint8_t* in, long long ip, int h, int w, float* out,
+                             long long op, cudaStream_t s) {
+  dim3 grid((w + 255) / 256, h < 65535 ? h : 65535);
+  u8_to_f32_kernel<<<grid, 256, 0, s>>>(in, ip, h, w, out, op);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const float* in, long long ip, int h, int w, uint8_t* out,
+                            long long op, cudaStream_t s) {
+  dim3 grid((w + 255) / 256, h < 65535 ? h : 65535);
+  quantize_kernel<<<grid, 256, 0, s>>>(in, ip, h, w, out, op);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_dwt2d(int kind, bool inverse, const T* in, long long ip, T* out,
                          long long op, int h, int w, cudaStream_t s) {

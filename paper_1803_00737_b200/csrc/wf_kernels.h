@@ -49,6 +49,14 @@ cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, bool tma, cuda
                         const LaunchTuning& tune);
 template <typename T>
 cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune);
+// 8 bpp: uint8 in, float32 arithmetic, quantised uint8 out (fuse.cu)
+template <>
+cudaError_t launch_fuse<uint8_t, float>(int kind, const FuseArgs<uint8_t>& a, bool vec, bool tma,
+                                        cudaStream_t s, const LaunchTuning& tune);
+cudaError_t launch_u8_to_f32(const uint8_t* in, long long ip, int h, int w, float* out,
+                             long long op, cudaStream_t s);
+cudaError_t launch_quantize(const float* in, long long ip, int h, int w, uint8_t* out,
+                            long long op, cudaStream_t s);
 
 // Standalone transforms (materialise coefficients; wavelet.py:131-164).
 template <typename T>

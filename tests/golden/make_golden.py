@@ -145,9 +145,47 @@ def metrics_golden():
     np.savez_compressed(OUT / "metrics.npz", **data)
 
 
+def quantized_golden():
+    """8 bpp path: the reference's worker computation on uint8 tiles,
+    [quantize(p) for p in fuse_tile_quantized(pan, ms, method)]
+    (tiling.py:163-172, 268-269; imageio.py:115-123), plus a whole
+    fuse_tiled(..., transfer_8bpp=True) run."""
+    from wavefuse import imageio, tiling
+
+    rng = np.random.default_rng(8)
+    data = {}
+    for k, (h, w, nb) in enumerate([(64, 96, 3), (32, 64, 2), (40, 128, 6), (16, 48, 1)]):
+        pan = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        ms = [rng.integers(0, 256, (h // 2, w // 2), dtype=np.uint8) for _ in range(nb)]
+        data[f"t{k}/pan"] = pan
+        for b, m in enumerate(ms):
+            data[f"t{k}/ms{b}"] = m
+        for kind in (HAAR, D4):
+            outs = [imageio.quantize(p)
+                    for p in tiling.fuse_tile_quantized(pan, ms, fusion.DwtReplace(kind))]
+            for b, o in enumerate(outs):
+                data[f"t{k}/{kind.value}/out{b}"] = o
+    pan = rng.uniform(0, 255, (64, 64)).astype(np.float32)
+    ms = [rng.uniform(0, 255, (32, 32)).astype(np.float32) for _ in range(3)]
+    grid = tiling.plan_grid(64, 64, 2, 2)
+    data["tiled/pan"] = pan
+    for b, m in enumerate(ms):
+        data[f"tiled/ms{b}"] = m
+    for kind in (HAAR, D4):
+        outs = tiling.fuse_tiled(pan, ms, fusion.DwtReplace(kind), grid, transfer_8bpp=True)
+        for b, o in enumerate(outs):
+            data[f"tiled/{kind.value}/out{b}"] = o
+    q = np.array([[-3.0, 0.49, 0.5, 1.5, 2.5], [254.5, 255.2, 300.0, 127.4999, 127.5]],
+                 dtype=np.float32)
+    data["quantize/in"] = q
+    data["quantize/out"] = imageio.quantize(q)
+    np.savez_compressed(OUT / "quantized.npz", **data)
+
+
 if __name__ == "__main__":
     fusion_golden()
     transform_golden()
     metrics_golden()
+    quantized_golden()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

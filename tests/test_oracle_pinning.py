@@ -10,6 +10,7 @@
 """
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -231,3 +232,18 @@ def test_parallel_cpu_baseline_is_exact(kind):
     got = O.fuse_parallel(pan, bands, kind, threads=3, strip_rows=48)
     for a, b in zip(got, ref):
         assert np.array_equal(a, b)
+
+
+def test_quantized_path_matches_reference_golden():
+    """8 bpp worker computation (tiling.py:163-172, 268-269) and quantize
+    (imageio.py:115-123), bit-exact against the reference's outputs."""
+    g = np.load(Path(__file__).parent / "golden" / "quantized.npz")
+    assert np.array_equal(O.quantize(g["quantize/in"]), g["quantize/out"])
+    for k in range(4):
+        nb = sum(1 for key in g.files if key.startswith(f"t{k}/ms"))
+        pan = g[f"t{k}/pan"]
+        ms = [g[f"t{k}/ms{b}"] for b in range(nb)]
+        for kind in KINDS:
+            got = O.fuse_quantized(pan, ms, kind)
+            for b, o in enumerate(got):
+                assert np.array_equal(o, g[f"t{k}/{kind}/out{b}"]), (k, kind, b)
