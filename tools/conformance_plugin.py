@@ -65,6 +65,21 @@ def _install():
     M.resample_bilinear = resample
     for name in ("degrade", "q_index", "ergas", "d_lambda", "d_s", "qnr"):
         setattr(M, name, translate(getattr(wf, name), name))
+    # a B200-backed cluster worker. WorkerServer.handle_task
+    # (cluster.py:297-299) is the reference's own hook; DWT tiles go to the GPU
+    # (8 bpp tile -> float32 planes, tiling.py:163-172), WA/IHS stay on the CPU.
+    import wavefuse.cluster as Cl
+
+    cpu_handle = Cl.WorkerServer.handle_task
+
+    def gpu_handle_task(self, tile, method):
+        if isinstance(method, F.DwtReplace):
+            ROUTED["worker_tiles"] = ROUTED.get("worker_tiles", 0) + 1
+            return wf.fuse_tile_quantized(tile.pan, tile.ms, wf.DwtReplace(kinds[method.kind]))
+        return cpu_handle(self, tile, method)
+
+    Cl.WorkerServer.handle_task = gpu_handle_task
+
     for name in ("fuse_dwt", "resample_bilinear", "dwt1d_forward", "dwt1d_inverse",
                  "dwt2d_forward", "dwt2d_inverse", "degrade", "q_index", "ergas", "d_lambda",
                  "d_s", "qnr"):
