@@ -179,6 +179,9 @@ def run_reference(args, rank: int):
     rate = args.cpu_rows * W * len(times) / 1e6 / sum(times)
     sample = (f"first {args.cpu_rows} PAN rows x {W} cols + 6 bands of the C2 scene per step, "
               f"oracle port of the reference (numpy f64, exact row strips)")
+    d4_steps = max(1, min(args.steps, 5))
+    d4_times = [cpu_sample("daub4", args.cpu_rows, threads)[1] for _ in range(d4_steps)]
+    d4_rate = args.cpu_rows * W * d4_steps / 1e6 / sum(d4_times)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -199,6 +202,10 @@ def run_reference(args, rank: int):
                          "sample": sample},
         "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "daub4": {"value": round(d4_rate, 3), "steps": d4_steps,
+                  "ms_per_step": round(1e3 * sum(d4_times) / d4_steps, 3),
+                  "cpu_baseline": {"value": round(d4_rate, 3), "unit": UNIT, "cores": threads,
+                                   "kind": "port", "sample": sample.replace("C2", "C3 (D4)")}},
     }
     print(json.dumps(line), flush=True)
 

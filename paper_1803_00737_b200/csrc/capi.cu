@@ -98,7 +98,8 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
     vec = vec && al16(out[b]) && al16(ms[b]);
   }
 
-  wf::LaunchTuning tune{0, 0, 0, 0};
+  wf::LaunchTuning tune{0, 0, 0, 0, 0};
+  if (const char* e = getenv("WF_HAAR_PPT")) tune.haar_ppt = atoi(e);
   if (const char* e = getenv("WF_D4_TARGET_WARPS")) tune.d4_target_warps = atoi(e);
   if (const char* e = getenv("WF_D4_MIN_PAIRS")) tune.d4_min_pairs = atoi(e);
   if (const char* e = getenv("WF_D4_PAIRS")) tune.d4_pairs = atoi(e);

@@ -254,9 +254,12 @@ __global__ void __launch_bounds__(kD4Threads)
 // pairs; PAN rows 2i, 2i+1 are loaded once and every band streams past them.
 // ---------------------------------------------------------------------------
 constexpr int kHaarThreads = 128;
-constexpr int kHaarPairsPerThread = 4;
+// one row pair per thread measured best (tools/sweep_haar.py: 6.56 TB/s at
+// B = 6 vs 6.28 at 4 pairs) -- more, shorter-lived warps keep more loads in flight
+constexpr int kHaarPairsPerThread = 1;
+constexpr int kHaarU8PairsPerThread = 4;
 
-template <typename T, typename Acc, int NB, bool kVec>
+template <typename T, typename Acc, int NB, bool kVec, int PPT>
 __global__ void __launch_bounds__(kHaarThreads)
     fuse_haar_kernel(const FuseArgs<T> a) {
   const int q = blockIdx.x * kHaarThreads + threadIdx.x;  // quad index
@@ -264,12 +267,12 @@ __global__ void __launch_bounds__(kHaarThreads)
   const int c = 4 * q;
   if (c >= W) return;
   const int npairs = a.rows >> 1;
-  const int i_begin = blockIdx.y * kHaarPairsPerThread;
+  const int i_begin = blockIdx.y * PPT;
   const bool full = kVec;  // W % 4 == 0 and pointers aligned (host-checked)
   const Acc quarter = Acc(0.25);
 
 #pragma unroll
-  for (int s = 0; s < kHaarPairsPerThread; ++s) {
+  for (int s = 0; s < PPT; ++s) {
     const int i = i_begin + s;
     if (i >= npairs) break;
     const T* r0 = a.pan + (long long)(2 * i) * a.pan_pitch;
@@ -328,12 +331,20 @@ static cudaError_t launch_nb(int kind, const FuseArgs<T>& a0, bool vec, cudaStre
   const int npairs = a.rows >> 1;
   if (kind == kHaar) {
     const int nq = (a.W + 3) / 4;
-    dim3 grid((nq + kHaarThreads - 1) / kHaarThreads,
-              (npairs + kHaarPairsPerThread - 1) / kHaarPairsPerThread);
-    if (vec)
-      fuse_haar_kernel<T, Acc, NB, true><<<grid, kHaarThreads, 0, s>>>(a);
-    else
-      fuse_haar_kernel<T, Acc, NB, false><<<grid, kHaarThreads, 0, s>>>(a);
+    const int ppt = tune.haar_ppt > 0 ? tune.haar_ppt : kHaarPairsPerThread;
+    dim3 grid((nq + kHaarThreads - 1) / kHaarThreads, (npairs + ppt - 1) / ppt);
+#define WF_HAAR_LAUNCH(P)                                                        \
+  if (vec)                                                                      \
+    fuse_haar_kernel<T, Acc, NB, true, P><<<grid, kHaarThreads, 0, s>>>(a);     \
+  else                                                                          \
+    fuse_haar_kernel<T, Acc, NB, false, P><<<grid, kHaarThreads, 0, s>>>(a);
+    switch (ppt) {
+      case 1: WF_HAAR_LAUNCH(1) break;
+      case 2: WF_HAAR_LAUNCH(2) break;
+      case 8: WF_HAAR_LAUNCH(8) break;
+      default: WF_HAAR_LAUNCH(4) break;
+    }
+#undef WF_HAAR_LAUNCH
     return cudaGetLastError();
   }
   // D4: choose the row-run length so that the task count fills the chip
@@ -400,9 +411,9 @@ __global__ void __launch_bounds__(kHaarThreads)
   const int c = 16 * g;
   if (c >= a.W) return;
   const int npairs = a.rows >> 1;
-  const int i_begin = blockIdx.y * kHaarPairsPerThread;
+  const int i_begin = blockIdx.y * kHaarU8PairsPerThread;
 #pragma unroll
-  for (int s = 0; s < kHaarPairsPerThread; ++s) {
+  for (int s = 0; s < kHaarU8PairsPerThread; ++s) {
     const int i = i_begin + s;
     if (i >= npairs) break;
     const uint8_t* r0 = a.pan + (long long)(2 * i) * a.pan_pitch + c;
@@ -473,7 +484,7 @@ template <int NB>
 static cudaError_t launch_haar_u8(const FuseArgs<uint8_t>& a, cudaStream_t s) {
   const int ng = (a.W + 15) / 16;
   dim3 grid((ng + kHaarThreads - 1) / kHaarThreads,
-            ((a.rows >> 1) + kHaarPairsPerThread - 1) / kHaarPairsPerThread);
+            ((a.rows >> 1) + kHaarU8PairsPerThread - 1) / kHaarU8PairsPerThread);
   fuse_haar_u8_kernel<NB><<<grid, kHaarThreads, 0, s>>>(a);
   return cudaGetLastError();
 }

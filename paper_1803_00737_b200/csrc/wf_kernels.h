@@ -40,6 +40,7 @@ struct LaunchTuning {
   int d4_min_pairs;     // <=0: no minimum
   int d4_pairs;         // >0: fixed row pairs per warp task (overrides the above)
   int d4_stages;        // >0: shared-memory ring depth of the TMA kernel
+  int haar_ppt;         // >0: Haar row pairs per thread (1, 2, 4, 8)
 };
 
 // vec: 16-byte vector path legal; tma: the bulk-copy D4 pipeline is legal
