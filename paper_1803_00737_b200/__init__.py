@@ -16,6 +16,7 @@ from .errors import (
     NotDivisible,
     OddDimension,
     OddLength,
+    OddTile,
     TooFewBands,
     TooShort,
     TooSmall,
@@ -33,6 +34,7 @@ from .fusion import (
     resample_bilinear,
 )
 from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, q_index, qnr
+from .tiling import TileGrid, fuse_tiled, padded_dims, plan_grid
 from .wavelet import (
     FilterBank,
     WaveletKind,
@@ -56,7 +58,9 @@ __all__ = [
     "NotDivisible",
     "OddDimension",
     "OddLength",
+    "OddTile",
     "QualityReport",
+    "TileGrid",
     "TooFewBands",
     "TooShort",
     "TooSmall",
@@ -76,7 +80,10 @@ __all__ = [
     "fuse_dwt",
     "fuse_quantized",
     "fuse_tile_quantized",
+    "fuse_tiled",
     "method_from_name",
+    "padded_dims",
+    "plan_grid",
     "q_index",
     "qnr",
     "quantize",

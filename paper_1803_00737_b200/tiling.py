@@ -1,0 +1,165 @@
+"""Tiled fusion with the reference's per-tile semantics, on the GPU
+(SURVEY.md 8(f) row f4).
+
+Drop-in for the DWT part of /root/reference/pkg/src/wavefuse/tiling.py:
+`TileGrid`, `plan_grid` (tiling.py:38-86) and `fuse_tiled` (tiling.py:213-273)
+with `workers` and `transfer_8bpp`. Every tile is fused as its own image --
+periodic wrap INSIDE the tile, the reference's documented choice "rather than
+add halo exchange" (tiling.py:1-12) -- by launching the fused
+kernel on a strided window of the device-resident scene (pitch = scene width),
+so no tile is ever copied. (For exact whole-scene results across GPUs use
+strips.py, which exchanges halos instead.)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .errors import BandCountMismatch, DimensionMismatch, NotDivisible, OddDimension, OddTile
+from .fusion import DwtReplace, FusionMethod, _quantize_dev, _u8_to_f32_dev, resample_bilinear
+from .wavelet import KIND_CODE, MIN_LEN, WaveletKind
+from .errors import TooSmall
+
+
+@dataclass(frozen=True)
+class TileGrid:
+    """tiling.py:38-58: equal-parts partition, sizes in pixels."""
+
+    grid_w: int
+    grid_h: int
+    pan_tile_w: int
+    pan_tile_h: int
+    ms_tile_w: int
+    ms_tile_h: int
+
+    @property
+    def tile_count(self) -> int:
+        return self.grid_w * self.grid_h
+
+    @property
+    def pan_w(self) -> int:
+        return self.grid_w * self.pan_tile_w
+
+    @property
+    def pan_h(self) -> int:
+        return self.grid_h * self.pan_tile_h
+
+
+def plan_grid(pan_w: int, pan_h: int, grid_w: int, grid_h: int) -> TileGrid:
+    """tiling.py:72-86"""
+    if grid_w < 1 or grid_h < 1:
+        raise ValueError(f"grid {grid_w}x{grid_h} must be at least 1x1")
+    if pan_w % grid_w or pan_h % grid_h:
+        raise NotDivisible(f"{pan_w}x{pan_h} not divisible into {grid_w}x{grid_h} tiles")
+    tile_w, tile_h = pan_w // grid_w, pan_h // grid_h
+    if tile_w % 2 or tile_h % 2:
+        raise OddTile(f"tile {tile_w}x{tile_h} has an odd dimension")
+    return TileGrid(grid_w, grid_h, tile_w, tile_h, tile_w // 2, tile_h // 2)
+
+
+def padded_dims(w: int, h: int, grid_w: int, grid_h: int) -> tuple[int, int]:
+    """tiling.py:276-285"""
+    if grid_w < 1 or grid_h < 1:
+        raise ValueError(f"grid {grid_w}x{grid_h} must be at least 1x1")
+    step_w, step_h = 2 * grid_w, 2 * grid_h
+    return (w + step_w - 1) // step_w * step_w, (h + step_h - 1) // step_h * step_h
+
+
+def _shape(x):
+    return tuple(x.shape) if isinstance(x, torch.Tensor) else np.shape(x)
+
+
+def _window_fuse(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
+                 out: list[torch.Tensor], grid: TileGrid) -> None:
+    """One fused launch per tile on strided windows of the device scene; each
+    tile wraps periodically within itself."""
+    lib = _native.load()
+    esz = pan.element_size()
+    fn = {torch.float32: lib.wf_fuse_bands_f32, torch.float64: lib.wf_fuse_bands_f64,
+          torch.uint8: lib.wf_fuse_bands_u8}[pan.dtype]
+    tw, th = grid.pan_tile_w, grid.pan_tile_h
+    pp, mp, op = pan.stride(0), ms[0].stride(0), out[0].stride(0)
+    s = _device.stream_ptr()
+    for row in range(grid.grid_h):
+        for col in range(grid.grid_w):
+            r0, c0 = row * th, col * tw
+            pan_p = pan.data_ptr() + (r0 * pp + c0) * esz
+            ms_p = _native.ptr_array([m.data_ptr() + ((r0 // 2) * mp + c0 // 2) * esz for m in ms])
+            out_p = _native.ptr_array([o.data_ptr() + (r0 * op + c0) * esz for o in out])
+            _native.check(fn(KIND_CODE[kind], pan_p, pp, ms_p, mp, out_p, op, len(ms), th, tw, s))
+
+
+def _u8_windows_ok(grid: TileGrid, kind: WaveletKind) -> bool:
+    mult = 16 if kind is WaveletKind.HAAR else 32
+    return grid.pan_tile_w % mult == 0 and grid.pan_w % 32 == 0
+
+
+def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
+               transfer_8bpp: bool = False):
+    """tiling.py:213-273 for DwtReplace. `workers` is accepted for signature
+    compatibility (the GPU fuses tiles, not a thread pool). Plain mode
+    resamples bands globally, then fuses every tile with per-tile wrap (float
+    output, pan dtype). transfer_8bpp reproduces the distributed pipeline:
+    inputs quantised to uint8 (wire_planes, tiling.py:192-210), each tile
+    fused in float32 and quantised (tiling.py:163-172, 268-269)."""
+    if workers < 1:
+        raise ValueError(f"workers {workers} must be >= 1")
+    is_t = isinstance(pan, torch.Tensor)
+    if not is_t:
+        pan = np.asarray(pan)
+    if _shape(pan) != (grid.pan_h, grid.pan_w):
+        raise DimensionMismatch(
+            f"panchromatic {_shape(pan)} does not match grid {grid.pan_w}x{grid.pan_h}")
+    bands = [b if isinstance(b, torch.Tensor) else np.asarray(b) for b in ms]
+    if not bands:
+        raise BandCountMismatch("need at least one band")
+    for b in bands[1:]:
+        if _shape(b) != _shape(bands[0]):
+            raise DimensionMismatch(f"band sizes differ: {_shape(b)} vs {_shape(bands[0])}")
+    if not isinstance(method, DwtReplace):
+        raise TypeError(f"unknown fusion method {method!r}")
+    kind = method.kind
+    th, tw = grid.pan_tile_h, grid.pan_tile_w
+    if th < MIN_LEN[kind] or tw < MIN_LEN[kind]:
+        raise TooSmall(f"{tw}x{th} below minimum {MIN_LEN[kind]} per side")
+    half = (grid.pan_h // 2, grid.pan_w // 2)
+
+    if transfer_8bpp:
+        # wire_planes: bands to half size (bilinear), then everything to uint8
+        low = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0]) for b in bands]
+
+        def to_u8(x):  # uint8 passes through; float planes are quantised (float32)
+            is_u8 = x.dtype == (torch.uint8 if isinstance(x, torch.Tensor) else np.uint8)
+            return _as_u8_dev(x) if is_u8 else _quantize_dev(_device.to_device(x, np.float32))
+
+        pan_u8 = to_u8(pan)
+        ms_u8 = [to_u8(b) for b in low]
+        if _u8_windows_ok(grid, kind):
+            outs = [torch.empty_like(pan_u8) for _ in ms_u8]
+            _window_fuse(kind, pan_u8, ms_u8, outs, grid)
+        else:  # same arithmetic through the float32 kernels + quantize
+            pan_f = _u8_to_f32_dev(pan_u8)
+            ms_f = [_u8_to_f32_dev(b) for b in ms_u8]
+            fo = [torch.empty_like(pan_f) for _ in ms_f]
+            _window_fuse(kind, pan_f, ms_f, fo, grid)
+            outs = [_quantize_dev(f) for f in fo]
+        return outs if is_t else [o.cpu().numpy() for o in outs]
+
+    dt = _device.np_out_dtype(pan)
+    sized = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0]) for b in bands]
+    pan_t = _device.to_device(pan, dt)
+    ms_t = [_device.to_device(b, dt) for b in sized]
+    outs = [torch.empty_like(pan_t) for _ in ms_t]
+    _window_fuse(kind, pan_t, ms_t, outs, grid)
+    return outs if is_t else [o.cpu().numpy() for o in outs]
+
+
+def _as_u8_dev(x) -> torch.Tensor:
+    dev = _device.require_cuda()
+    if isinstance(x, torch.Tensor):
+        return (x if x.is_cuda else x.to(dev)).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)

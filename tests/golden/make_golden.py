@@ -182,10 +182,35 @@ def quantized_golden():
     np.savez_compressed(OUT / "quantized.npz", **data)
 
 
+def tiled_golden():
+    """tiling.fuse_tiled (tiling.py:213-273): per-tile periodic wrap, plain
+    (float) mode, including bands that need the global resample first."""
+    from wavefuse import tiling
+
+    rng = np.random.default_rng(12)
+    data = {}
+    cases = [("g0", 64, 96, 3, 2, 2, (32, 48)), ("g1", 64, 128, 2, 4, 2, (32, 64)),
+             ("g2", 48, 48, 2, 3, 3, (24, 24)), ("g3", 40, 80, 2, 2, 2, (13, 21))]
+    for name, h, w, nb, gw, gh, mshape in cases:
+        pan = rng.uniform(0, 255, (h, w)).astype(np.float32)
+        ms = [rng.uniform(0, 255, mshape).astype(np.float32) for _ in range(nb)]
+        data[f"{name}/pan"] = pan
+        data[f"{name}/grid"] = np.array([gw, gh])
+        for b, m in enumerate(ms):
+            data[f"{name}/ms{b}"] = m
+        grid = tiling.plan_grid(w, h, gw, gh)
+        for kind in (HAAR, D4):
+            outs = tiling.fuse_tiled(pan, ms, fusion.DwtReplace(kind), grid, workers=2)
+            for b, o in enumerate(outs):
+                data[f"{name}/{kind.value}/out{b}"] = o
+    np.savez_compressed(OUT / "tiled.npz", **data)
+
+
 if __name__ == "__main__":
     fusion_golden()
     transform_golden()
     metrics_golden()
     quantized_golden()
+    tiled_golden()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -118,3 +118,21 @@ def test_product_never_imports_oracle():
                 assert not any(a.name.split(".")[0] == "oracle" for a in node.names), py
             if isinstance(node, ast.ImportFrom):
                 assert (node.module or "").split(".")[0] != "oracle", py
+
+
+def test_plan_grid_contract():
+    """tiling.py:72-86, 276-285 (test_tiling.py:20-60)"""
+    g = wf.plan_grid(64, 32, 4, 2)
+    assert (g.pan_tile_w, g.pan_tile_h, g.ms_tile_w, g.ms_tile_h) == (16, 16, 8, 8)
+    assert g.tile_count == 8 and g.pan_w == 64 and g.pan_h == 32
+    with pytest.raises(errors.NotDivisible):
+        wf.plan_grid(30, 30, 4, 4)
+    with pytest.raises(errors.OddTile):
+        wf.plan_grid(30, 30, 2, 2)
+    with pytest.raises(ValueError):
+        wf.plan_grid(8, 8, 0, 1)
+    assert wf.padded_dims(30, 30, 4, 4) == (32, 32)
+    with pytest.raises(errors.DimensionMismatch):
+        wf.fuse_tiled(np.ones((8, 8)), [np.ones((4, 4))], wf.DwtReplace(H), g)
+    with pytest.raises(ValueError):
+        wf.fuse_tiled(np.ones((32, 64)), [np.ones((16, 32))], wf.DwtReplace(H), g, workers=0)
