@@ -94,8 +94,9 @@ def _window_fuse(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
 
 
 def _u8_windows_ok(grid: TileGrid, kind: WaveletKind) -> bool:
-    mult = 16 if kind is WaveletKind.HAAR else 32
-    return grid.pan_tile_w % mult == 0 and grid.pan_w % 32 == 0
+    # the 8 bpp kernels need 16-byte aligned PAN and MS window bases and row
+    # pitches: tile widths (hence MS tile widths x2) that are multiples of 32
+    return grid.pan_tile_w % 32 == 0 and grid.pan_w % 32 == 0
 
 
 def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
