@@ -99,6 +99,14 @@ __device__ __forceinline__ float lane_sum32(const float* p) {
   return (v[0].x + v[0].y) + (v[0].z + v[0].w);
 }
 
+// Knuth TwoSum: s + t == a + b exactly (the library is built with
+// -fmad=false, so nothing here is contracted or reassociated).
+__device__ __forceinline__ void two_sum(float a, float b, float& s, float& t) {
+  s = a + b;
+  const float bb = s - a;
+  t = (a - (s - bb)) + (b - bb);
+}
+
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -214,10 +222,13 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
 
   // low-res shifts of a tile: the low-res block's first MS pixel and first
   // degraded PAN pixel; loaded one tile ahead so their latency is hidden
-  auto load_shifts = [&](int tile, float (&kmv)[NB], double& kpdv) {
+  // The degraded-PAN shift is kept as the exact float pair (hi, lo) of its
+  // 2x2 sum, formed by the same TwoSum sequence the main loop uses, so a
+  // constant region gives exactly zero deltas.
+  auto load_shifts = [&](int tile, float (&kmv)[NB], float& kph, float& kpl) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) kmv[k] = 0.f;
-    kpdv = 0.0;
+    kph = kpl = 0.f;
     if (tile >= ntiles) return;
     const int br = tile / a.ncx, cx = tile % a.ncx;
     const int bc = cx * kQsWarps + warp;
@@ -227,14 +238,16 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
 #pragma unroll
     for (int k = 0; k < NB; ++k)
       kmv[k] = __ldg(a.M[k] + min(my, (long long)a.Hh - 1) * a.mp + min(mx, (long long)a.Wh - 1));
-    if (py + 1 < a.H && px + 1 < a.W)
-      kpdv = ((double)__ldg(a.P + py * a.pp + px) + (double)__ldg(a.P + py * a.pp + px + 1) +
-              (double)__ldg(a.P + (py + 1) * a.pp + px) +
-              (double)__ldg(a.P + (py + 1) * a.pp + px + 1)) * 0.25;
+    if (py + 1 < a.H && px + 1 < a.W) {
+      float s, t, s2, t2, T;
+      two_sum(__ldg(a.P + py * a.pp + px), __ldg(a.P + (py + 1) * a.pp + px), s, t);
+      two_sum(__ldg(a.P + py * a.pp + px + 1), __ldg(a.P + (py + 1) * a.pp + px + 1), s2, t2);
+      two_sum(s, s2, kph, T);
+      kpl = T + (t + t2);
+    }
   };
-  float km_next[NB];
-  double kpd_next;
-  load_shifts(blockIdx.x, km_next, kpd_next);
+  float km_next[NB], kph_next, kpl_next;
+  load_shifts(blockIdx.x, km_next, kph_next, kpl_next);
 
   int g = 0;
   int parity = 0;
@@ -258,16 +271,19 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
     const bool low_ok = blk_ok && lr < a.nbr_l && lc < a.nbc_l;
 
     float km[NB];
-    double kpd = kpd_next;
+    const float kph = kph_next, kpl = kpl_next;
 #pragma unroll
     for (int k = 0; k < NB; ++k) km[k] = km_next[k];
 
     float2 a1[NB];      // (sum dF_k, sum dU_k)
     float2 a2[L::NFF];  // (sum dF_k dF_l, sum dU_k dU_l), k <= l
-    float2 ax[NB];      // (sum dF_k dU_k, sum dF_k dP)
+    float axu[NB], axp[NB];  // sum dF_k dU_k, sum dF_k dP (scalar FFMA: no operand packing)
     float a1p = 0.f, app = 0.f;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) a1[k] = ax[k] = make_float2(0.f, 0.f);
+    for (int k = 0; k < NB; ++k) {
+      a1[k] = make_float2(0.f, 0.f);
+      axu[k] = axp[k] = 0.f;
+    }
 #pragma unroll
     for (int k = 0; k < L::NFF; ++k) a2[k] = make_float2(0.f, 0.f);
     float kf[NB], ku[NB], kp = 0.f;
@@ -285,7 +301,7 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
 
     for (int t = 0; t < 16; ++t, ++g) {
       const int s = g % S;
-      if (t == 8) load_shifts(tile + gridDim.x, km_next, kpd_next);
+      if (t == 8) load_shifts(tile + gridDim.x, km_next, kph_next, kpl_next);
       tma::mbar_wait(&full[s], (g / S) & 1);
       const float* slot = ring + (size_t)s * C::SLOT;
       const float* msr = slot + C::MSOFF;
@@ -344,24 +360,32 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
         for (int k = 0; k < NB; ++k) {
 #pragma unroll
           for (int l = k; l < NB; ++l) a2[L::tri(k, l)] = __ffma2_rn(d[k], d[l], a2[L::tri(k, l)]);
-          ax[k] = __ffma2_rn(make_float2(d[k].x, d[k].x), make_float2(d[k].y, dp), ax[k]);
+          axu[k] = fmaf(d[k].x, d[k].y, axu[k]);
+          axp[k] = fmaf(d[k].x, dp, axp[k]);
         }
       }
 
-      // 2x2 cells: degraded F and P (float64, exact for float32 data)
+      // 2x2 cells: degraded F and P as the EXACT float pair (hi, lo) of the
+      // 4-pixel sum (TwoSum per column, exchange with the odd neighbour lane,
+      // TwoSum of the two columns); even lanes own the cell. No float64, no
+      // conversions: e = hi/4 - m + lo/4 is exact to one rounding and exactly
+      // zero whenever degrade(F) == M (Haar).
       {
-        double sp = (double)pv[0] + (double)pv[1];
-        sp += __shfl_xor_sync(0xffffffffu, sp, 1);
-        const double pd = sp * 0.25;
-        const float dpd = (float)(pd - kpd);
+        float s, t, S, T;
+        two_sum(pv[0], pv[1], s, t);
+        two_sum(s, __shfl_xor_sync(0xffffffffu, s, 1), S, T);
+        const float plo = T + (t + __shfl_xor_sync(0xffffffffu, t, 1));
+        // (kph, kpl) = the low-res block origin's (hi, lo), unscaled
+        const float dpd = 0.25f * ((S - kph) + (plo - kpl));
         lw[NB] += dpd;
         lw[2 * NB + 1] = fmaf(dpd, dpd, lw[2 * NB + 1]);
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-          double sf = (double)fv[0][k] + (double)fv[1][k];
-          sf += __shfl_xor_sync(0xffffffffu, sf, 1);
-          const double e = sf * 0.25 - (double)rawc[k];  // rawc = M_k(i, x/2) on even lanes
-          sse[k] += (float)(e * e);
+          two_sum(fv[0][k], fv[1][k], s, t);
+          two_sum(s, __shfl_xor_sync(0xffffffffu, s, 1), S, T);
+          const float lo = T + (t + __shfl_xor_sync(0xffffffffu, t, 1));
+          const float e = fmaf(S, 0.25f, -rawc[k]) + 0.25f * lo;  // rawc = M_k(i, x/2), even lanes
+          sse[k] = fmaf(e, e, sse[k]);
           summ[k] += rawc[k];
           const float dm = rawc[k] - km[k];
           lw[k] += dm;
@@ -390,8 +414,8 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
       for (int k = 0; k < NB; ++k) {
         tr[k * kTrPad + lane] = a1[k].x;
         tr[(NB + k) * kTrPad + lane] = a1[k].y;
-        tr[(L::NP + 2 * L::NFF + k) * kTrPad + lane] = ax[k].x;
-        tr[(L::NP + 2 * L::NFF + NB + k) * kTrPad + lane] = ax[k].y;
+        tr[(L::NP + 2 * L::NFF + k) * kTrPad + lane] = axu[k];
+        tr[(L::NP + 2 * L::NFF + NB + k) * kTrPad + lane] = axp[k];
       }
       tr[2 * NB * kTrPad + lane] = a1p;
 #pragma unroll
@@ -462,11 +486,14 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
       }
       const double* lowv = ds + L::NT;
       if (low_ok) {
-        double* dst = part_low + ((size_t)(lr * a.nbc_l + lc) * 4 + (br & 1) * 2 + (bc & 1)) *
-                                     (L::NLOW + NB + 1);
-        for (int k = lane; k < L::NLOW; k += 32) dst[k] = lowv[k];
-        if (lane < NB) dst[L::NLOW + lane] = ds[L::NV + L::NP + lane];
-        if (lane == 0) dst[L::NLOW + NB] = kpd;
+        // field-major layout [quarter][field][low-res block]: the finish
+        // kernel reads each field contiguously
+        const size_t nlow = (size_t)a.nbr_l * a.nbc_l;
+        double* dst = part_low + (size_t)((br & 1) * 2 + (bc & 1)) * (L::NLOW + NB + 1) * nlow +
+                      (size_t)(lr * a.nbc_l + lc);
+        for (int k = lane; k < L::NLOW; k += 32) dst[k * nlow] = lowv[k];
+        if (lane < NB) dst[(L::NLOW + lane) * nlow] = ds[L::NV + L::NP + lane];
+        if (lane == 0) dst[(L::NLOW + NB) * nlow] = (double)kph * 0.25 + (double)kpl * 0.25;
       }
       for (int k = lane; k < L::NERG; k += 32)
         ewp[warp * L::NERG + k] = blk_ok ? lowv[L::NLOW + k] : 0.0;
@@ -479,12 +506,12 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
       for (int q = lane; q < L::NQ; q += 32) {
         double v = 0.0;
         for (int w = 0; w < kQsWarps; ++w) v += qwp[w * L::NQ + q];
-        part_q[(size_t)tile * L::NQ + q] = v;
+        part_q[(size_t)q * ntiles + tile] = v;  // quantity-major: coalesced finish
       }
       for (int q = lane; q < L::NERG; q += 32) {
         double v = 0.0;
         for (int w = 0; w < kQsWarps; ++w) v += ewp[w * L::NERG + q];
-        part_erg[(size_t)tile * L::NERG + q] = v;
+        part_erg[(size_t)q * ntiles + tile] = v;
       }
     }
   }
@@ -535,7 +562,7 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x < 2 * NB) {
     double v = 0.0;
     for (int w = 0; w < 8; ++w) v += red[threadIdx.x * 8 + w];
-    part[(size_t)blockIdx.x * 2 * NB + threadIdx.x] = v;
+    part[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
   }
 }
 
@@ -561,32 +588,33 @@ __global__ void __launch_bounds__(1024)
   const int q = blockIdx.x;
   double v = 0.0;
   if (q < L::NQ) {
-    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_q[(size_t)c * L::NQ + q];
+    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_q[(size_t)q * ncta + c];
     v = block_sum(v);
     if (threadIdx.x == 0) out[q] = v / ((double)a.nbr * a.nbc);
   } else if (q < L::NQ + NB) {
     const int k = q - L::NQ;
     const int nlow = a.nbr_l * a.nbc_l;
     for (int b = threadIdx.x; b < nlow; b += blockDim.x) {
-      const double* src = part_low + (size_t)b * 4 * (L::NLOW + NB + 1);
+      const size_t nl = (size_t)nlow, qs = (size_t)(L::NLOW + NB + 1) * nl;
+      const double* src = part_low + b;
       double s1m = 0, s1p = 0, smm = 0, spp = 0, smp = 0;
       for (int qd = 0; qd < 4; ++qd) {
-        const double* p = src + qd * (L::NLOW + NB + 1);
-        s1m += p[k];
-        s1p += p[NB];
-        smm += p[NB + 1 + k];
-        spp += p[2 * NB + 1];
-        smp += p[2 * NB + 2 + k];
+        const double* p = src + qd * qs;
+        s1m += p[k * nl];
+        s1p += p[NB * nl];
+        smm += p[(NB + 1 + k) * nl];
+        spp += p[(2 * NB + 1) * nl];
+        smp += p[(2 * NB + 2 + k) * nl];
       }
-      v += q_from_sums(1024.0, src[L::NLOW + k], src[L::NLOW + NB], s1m, s1p, smm, spp, smp,
+      v += q_from_sums(1024.0, src[(L::NLOW + k) * nl], src[(L::NLOW + NB) * nl], s1m, s1p, smm, spp, smp,
                        undecidable);
     }
     v = block_sum(v);
     if (threadIdx.x == 0) out[q] = v / (double)nlow;
   } else {
     const int e = q - L::NQ - NB;  // 0..2NB-1: sse_k then sum_k
-    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_erg[(size_t)c * 2 * NB + e];
-    for (int c = threadIdx.x; c < nedge; c += blockDim.x) v += part_edge[(size_t)c * 2 * NB + e];
+    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_erg[(size_t)e * ncta + c];
+    for (int c = threadIdx.x; c < nedge; c += blockDim.x) v += part_edge[(size_t)e * nedge + c];
     v = block_sum(v);
     if (threadIdx.x == 0) out[q] = v / ((double)a.Hh * a.Wh);
   }
