@@ -291,6 +291,56 @@ def measure_e2e(scene, kind, steps, dist):
     return sec, h2d, d2h, ok
 
 
+def measure_quality(scene, steps, warmup, peak):
+    """North-star subsystem (b): the full QNR/ERGAS report of the fused Haar
+    scene (one-pass scene kernel + edge + finish launches), CUDA-event time
+    per report. Algorithmic bytes: fused bands + MS + PAN read once."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind, _device, _native
+
+    lib = _native.load()
+    scene.launcher(WaveletKind.HAAR)()
+    h, w = scene.shape
+    nb = len(scene.ms)
+    ws = torch.empty(int(lib.wf_quality_scene_workspace_bytes(nb, h, w)) // 8 + 1,
+                     dtype=torch.float64, device="cuda")
+    out = torch.zeros(64, dtype=torch.float64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fp = _native.ptr_array([t.data_ptr() for t in scene.out])
+    mp = _native.ptr_array([t.data_ptr() for t in scene.ms])
+
+    def run():
+        _native.check(lib.wf_quality_scene_f32(fp, mp, scene.pan.data_ptr(), w, w // 2, w, nb, h,
+                                               w, ws.data_ptr(), out.data_ptr(),
+                                               flag.data_ptr(), _device.stream_ptr()))
+
+    for _ in range(warmup):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(3, min(steps, 20))
+    e0.record()
+    for _ in range(n):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    per = e0.elapsed_time(e1) / n
+    import paper_1803_00737_b200 as wf
+
+    rep = wf.qnr(scene.out, scene.ms, scene.pan)
+    nbytes = (4 * nb + 4) * h * w + nb * (h // 2) * (w // 2) * 4
+    achieved = nbytes / (per * 1e-3) / 1e9
+    return {
+        "ms_per_report": round(per, 4),
+        "report": {"ergas": rep.ergas, "qnr": rep.qnr, "d_lambda": rep.d_lambda, "d_s": rep.d_s},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "algorithmic_bytes_per_report": nbytes,
+                     "kernels": "quality_scene_kernel<6> + quality_edge_kernel + quality_finish"},
+        "reference_cpu_estimate": "qnr() at 4096^2 x 6 bands: 47 s single-thread (SURVEY.md S5)",
+    }
+
+
 def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
     """the same scene in the paper's 8 bpp transfer
     representation (uint8 in, quantised uint8 out, float32 arithmetic). A
@@ -399,6 +449,7 @@ def run_ours(args, rank, world, local_rank):
             },
         }
     u8 = measure_u8(scene, args.steps, args.warmup, dist, world, local_rank, peak)
+    quality = measure_quality(scene, args.steps, args.warmup, peak)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -446,6 +497,7 @@ def run_ours(args, rank, world, local_rank):
                 "cpu_baseline": cpu.get("daub4"),
             },
             "u8_8bpp": u8,
+            "quality": quality,
         }
         print(json.dumps(line), flush=True)
     if dist:
