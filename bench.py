@@ -60,6 +60,9 @@ def parse():
                          "NCCL halo exchange inside every step")
     ap.add_argument("--strip-size", type=int, default=65536)
     ap.add_argument("--scenes", type=int, default=64, help="batch64: scenes in the batch")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="strip65536: D4 halo rows read from the neighbours' HBM through CUDA "
+                         "IPC inside the kernel (peer) or exchanged by NCCL send/recv each step")
     return ap.parse_args()
 
 
@@ -529,9 +532,13 @@ def run_strips(args, rank, world, local_rank):
     synth.device_plane(ms, synth.DEFAULT_SEED, synth.plane_id(0, 0), row0=r0 // 2)
     out = [torch.empty_like(pan)]
     kind = WaveletKind.DAUB4
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()  # all strips exist before neighbours map them
+    peer = strips.PeerHalos(pan, [ms]) if args.halo == "peer" else None
 
     def step():
-        halos = strips.exchange_halos(pan, [ms])
+        halos = peer if peer is not None else strips.exchange_halos(pan, [ms])
         strips.fuse_strip(kind, pan, [ms], halos, out)
 
     for _ in range(args.warmup):
@@ -561,6 +568,10 @@ def run_strips(args, rank, world, local_rank):
     strip_bytes = scene_bytes(rows, n, 1)
     per_launch = ms_t / args.steps
     achieved = strip_bytes / (per_launch * 1e-3) / 1e9
+    if dist:
+        dist.barrier()  # neighbours finished reading before the mappings go away
+    if peer is not None:
+        peer.close()
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -576,7 +587,10 @@ def run_strips(args, rank, world, local_rank):
             "dtype": "f32",
             "data": "synthetic (device counter-hash uniform[0,255) f32)",
             "config": {"workload": f"C4: one {n}x{n} PAN + 1 MS band, D4 periodic wrap, "
-                                   f"row strips of {rows} rows per rank, NCCL halo ring",
+                                   f"row strips of {rows} rows per rank",
+                       "halo": ("peer: neighbours' halo rows bulk-copied from their HBM by the "
+                                "strip kernel (CUDA IPC over NVLink), no collective per step")
+                       if args.halo == "peer" else "nccl: batched send/recv ring each step",
                        "global_batch": 1, "parallelism": f"row strips x{world}",
                        "l2": "no flush: inputs >> 126 MB L2"},
             "gpu_launches": launches,

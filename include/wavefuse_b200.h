@@ -208,6 +208,16 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
                          int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
                          int w, void* workspace, double* out, int* undecidable, void* stream);
 
+/* ---- peer-memory halos for strip-sharded scenes (one process per GPU) ----
+ * wf_ipc_export: 64-byte CUDA IPC handle of the allocation containing `ptr`
+ * and the byte offset of `ptr` in it. wf_ipc_open: map a neighbour's handle
+ * (lazy peer access over NVLink); pass base + offset + row * pitch as the
+ * pan_top / pan_bot / ms_top halo pointers of wf_fuse_strip_*, whose producer
+ * then copies the halo rows straight out of peer HBM. */
+int wf_ipc_export(const void* ptr, void* handle64, uint64_t* offset);
+int wf_ipc_open(const void* handle64, void** base);
+int wf_ipc_close(void* base);
+
 /* ---- synthetic scenes (counter hash; numpy twin in synth.py) ------------ */
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
                        uint32_t plane, int row0, int col0, void* stream);

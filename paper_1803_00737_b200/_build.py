@@ -58,6 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp)]
     cmd += [str(s) for s in sources()]
+    cmd += ["-ldl"]  # peer.cu resolves cuMemGetAddressRange from libcuda at run time
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)

@@ -724,6 +724,16 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
   return cuda_status(e, "wf_quality_scene_f32");
 }
 
+int wf_ipc_export(const void* ptr, void* handle64, uint64_t* offset) {
+  if (!ptr || !handle64 || !offset) return fail(WF_ERR_VALUE, "null pointer argument");
+  return cuda_status(wf::ipc_export(ptr, handle64, offset), "wf_ipc_export");
+}
+int wf_ipc_open(const void* handle64, void** base) {
+  if (!handle64 || !base) return fail(WF_ERR_VALUE, "null pointer argument");
+  return cuda_status(wf::ipc_open(handle64, base), "wf_ipc_open");
+}
+int wf_ipc_close(void* base) { return cuda_status(wf::ipc_close(base), "wf_ipc_close"); }
+
 int wf_synth_plane_f32(float* out, int64_t pitch, int rows, int cols, uint64_t seed,
                        uint32_t plane, int row0, int col0, void* stream) {
   if (!out || rows < 0 || cols < 0 || pitch < cols)

@@ -92,6 +92,11 @@ cudaError_t launch_quality_scene(int nb, const float* const* F, const float* con
                                  int w, void* workspace, double* out, int* undecidable,
                                  cudaStream_t s);
 
+// CUDA IPC for the peer-memory halo path (peer.cu)
+cudaError_t ipc_export(const void* ptr, void* handle64, uint64_t* offset);
+cudaError_t ipc_open(const void* handle64, void** base);
+cudaError_t ipc_close(void* base);
+
 // Counter-hash synthetic plane (uniform [0,255) f32), numpy twin in
 // paper_1803_00737_b200/synth.py.
 cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsigned long long seed,

@@ -20,6 +20,7 @@ Halo volume per rank: 4 PAN rows + B MS rows, e.g. 1.1 MiB at W = 65536 —
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable, Sequence
 
 import torch
@@ -82,20 +83,89 @@ def exchange_halos(pan: torch.Tensor, ms: list[torch.Tensor], group=None):
     return pan_top, pan_bot, ms_top
 
 
+class PeerHalos:
+    """D4 halo rows read straight from the ring neighbours' HBM (CUDA IPC over
+    NVLink, one process per GPU on one node) instead of being exchanged.
+
+    Built once per strip-sharded scene: every rank exports the allocations
+    holding its PAN and MS strips (wf_ipc_export), the 64-byte handles are
+    all-gathered once, and each rank maps its two neighbours (wf_ipc_open).
+    The halo "buffers" are then just pointers into the neighbours' strips:
+    PAN rows rows-2, rows-1 of rank g-1, rows 0, 1 of rank g+1, and the last
+    MS row of every band of rank g-1. wf_fuse_strip_*'s producer warp
+    bulk-copies those rows over NVLink tile by tile, so a fusion step contains
+    no collective at all. The inputs must not change while neighbours may be
+    reading them (they are fusion inputs, written once before the steps)."""
+
+    def __init__(self, pan: torch.Tensor, ms: list[torch.Tensor], group=None):
+        self._opened: list[int] = []
+        es = pan.element_size()
+        rows, pitch = pan.shape[0], pan.stride(0)
+        mrows, mpitch = ms[0].shape[0], ms[0].stride(0)
+        self.halo_pitch = pitch
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if world == 1:  # periodic wrap onto this strip itself
+            self.pan_top = pan.data_ptr() + (rows - 2) * pitch * es
+            self.pan_bot = pan.data_ptr()
+            self.ms_top = [m.data_ptr() + (mrows - 1) * mpitch * es for m in ms]
+            return
+        lib = _native.load()
+
+        def export(t: torch.Tensor):
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_uint64()
+            _native.check(lib.wf_ipc_export(t.data_ptr(), h, ctypes.byref(off)))
+            return bytes(h), int(off.value)
+
+        mine = {"pan": export(pan), "ms": [export(m) for m in ms], "rows": rows, "mrows": mrows}
+        table: list = [None] * world
+        dist.all_gather_object(table, mine, group)
+        rank = dist.get_rank(group)
+        prev, nxt = table[(rank - 1) % world], table[(rank + 1) % world]
+        bases: dict[bytes, int] = {}
+
+        def open_(h: bytes) -> int:  # each allocation is mapped once per process
+            if h not in bases:
+                base = ctypes.c_void_p()
+                _native.check(lib.wf_ipc_open(h, ctypes.byref(base)))
+                bases[h] = base.value
+                self._opened.append(base.value)
+            return bases[h]
+
+        ph, po = prev["pan"]
+        nh, no = nxt["pan"]
+        self.pan_top = open_(ph) + po + (prev["rows"] - 2) * pitch * es
+        self.pan_bot = open_(nh) + no
+        self.ms_top = [open_(h) + o + (prev["mrows"] - 1) * mpitch * es for h, o in prev["ms"]]
+
+    def close(self) -> None:
+        lib = _native.load()
+        for b in self._opened:
+            lib.wf_ipc_close(b)
+        self._opened.clear()
+
+
+def _halo_pointers(halos):
+    """(pan_top, pan_bot, halo_pitch, [ms_top]) from exchange_halos tensors or
+    a PeerHalos mapping."""
+    if isinstance(halos, PeerHalos):
+        return halos.pan_top, halos.pan_bot, halos.halo_pitch, halos.ms_top
+    top, bot, mtop = halos
+    return top.data_ptr(), bot.data_ptr(), top.stride(0), [m.data_ptr() for m in mtop]
+
+
 def fuse_strip(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
                halos=None, out: list[torch.Tensor] | None = None) -> list[torch.Tensor]:
     """Fuse one row strip on this rank's GPU through wf_fuse_strip_*.
-    `halos` = exchange_halos(...) result (required for D4)."""
+    `halos` = exchange_halos(...) tensors or a PeerHalos mapping (D4)."""
     rows, w = pan.shape
     if out is None:
         out = [torch.empty_like(pan) for _ in ms]
     lib = _native.load()
     fn = lib.wf_fuse_strip_f32 if pan.dtype == torch.float32 else lib.wf_fuse_strip_f64
     if kind is WaveletKind.DAUB4:
-        top, bot, mtop = halos
-        top_p, bot_p = top.data_ptr(), bot.data_ptr()
-        mtop_p = _native.ptr_array([m.data_ptr() for m in mtop])
-        hp = top.stride(0)
+        top_p, bot_p, hp, mtops = _halo_pointers(halos)
+        mtop_p = _native.ptr_array(mtops)
     else:
         top_p = bot_p = None
         mtop_p = None
