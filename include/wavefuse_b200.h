@@ -106,6 +106,18 @@ int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const doub
                       const double* const* ms_top, int64_t ms_pitch, double* const* out,
                       int64_t out_pitch, int nbands, int rows, int w, void* stream);
 
+/* Reference-exact fuse_dwt (fusion.py:148-150 step by step): float64
+ * forward transform in the reference's operation order, LL <- band * gain,
+ * float64 inverse, one final cast -- bit-identical to the reference for f32
+ * and f64 callers. Three launches and an h*w float64 coefficient workspace
+ * (8*h*w bytes, caller-owned), so ~5x the HBM traffic of wf_fuse_dwt_*. */
+int wf_fuse_dwt_exact_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,
+                          int64_t ms_pitch, float* out, int64_t out_pitch, int h, int w,
+                          void* workspace, void* stream);
+int wf_fuse_dwt_exact_f64(int kind, const double* pan, int64_t pan_pitch, const double* ms,
+                          int64_t ms_pitch, double* out, int64_t out_pitch, int h, int w,
+                          void* workspace, void* stream);
+
 /* ---- fused hot path (HOST buffers, contiguous rows) --------------------- */
 typedef struct wf_ctx wf_ctx;
 /* strip_rows: PAN rows per pipeline stage (even; 0 = default 512). */

@@ -46,9 +46,9 @@ __device__ __forceinline__ double inv_tap(int kind, const D4& t, int p, double a
 // ---- 2D forward: rows then columns (wavelet.py:149-155) -------------------
 // One thread per coefficient position (i, j) of the half-size grid; it writes
 // LL(i,j), HL(i, Wh+j), LH(Hh+i, j), HH(Hh+i, Wh+j).
-template <typename T>
+template <typename T, typename To = T>
 __global__ void dwt2d_forward_kernel(int kind, const T* __restrict__ in, long long ip,
-                                     T* __restrict__ out, long long op, int H, int W) {
+                                     To* __restrict__ out, long long op, int H, int W) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y * blockDim.y + threadIdx.y;
   const int Hh = H >> 1, Wh = W >> 1;
@@ -65,17 +65,17 @@ __global__ void dwt2d_forward_kernel(int kind, const T* __restrict__ in, long lo
     d[k] = fwd_hi(kind, t, x[0], x[1], x[2], x[3]);
   }
   if (kind == kHaar) a[2] = a[3] = d[2] = d[3] = 0.0;
-  out[(long long)i * op + j] = (T)fwd_lo(kind, t, a[0], a[1], a[2], a[3]);
-  out[(long long)i * op + Wh + j] = (T)fwd_lo(kind, t, d[0], d[1], d[2], d[3]);
-  out[(long long)(Hh + i) * op + j] = (T)fwd_hi(kind, t, a[0], a[1], a[2], a[3]);
-  out[(long long)(Hh + i) * op + Wh + j] = (T)fwd_hi(kind, t, d[0], d[1], d[2], d[3]);
+  out[(long long)i * op + j] = (To)fwd_lo(kind, t, a[0], a[1], a[2], a[3]);
+  out[(long long)i * op + Wh + j] = (To)fwd_lo(kind, t, d[0], d[1], d[2], d[3]);
+  out[(long long)(Hh + i) * op + j] = (To)fwd_hi(kind, t, a[0], a[1], a[2], a[3]);
+  out[(long long)(Hh + i) * op + Wh + j] = (To)fwd_hi(kind, t, d[0], d[1], d[2], d[3]);
 }
 
 // ---- 2D inverse: columns then rows (wavelet.py:158-164) -------------------
 // One thread per output 2x2 block (i, j).
-template <typename T>
+template <typename T, typename To = T>
 __global__ void dwt2d_inverse_kernel(int kind, const T* __restrict__ in, long long ip,
-                                     T* __restrict__ out, long long op, int H, int W) {
+                                     To* __restrict__ out, long long op, int H, int W) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y * blockDim.y + threadIdx.y;
   const int Hh = H >> 1, Wh = W >> 1;
@@ -95,10 +95,22 @@ __global__ void dwt2d_inverse_kernel(int kind, const T* __restrict__ in, long lo
     cv[1][k] = inv_tap(kind, t, 1, ap, dp, a, d);
   }
   for (int p = 0; p < 2; ++p) {
-    T* row = out + (long long)(2 * i + p) * op;
-    row[2 * j] = (T)inv_tap(kind, t, 0, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
-    row[2 * j + 1] = (T)inv_tap(kind, t, 1, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
+    To* row = out + (long long)(2 * i + p) * op;
+    row[2 * j] = (To)inv_tap(kind, t, 0, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
+    row[2 * j + 1] = (To)inv_tap(kind, t, 1, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
   }
+}
+
+// ---- reference-exact fusion (fusion.py:148-150 step by step) ---------------
+// coeffs[:h/2, :w/2] = band.astype(f64) * gain  (fusion.py:149)
+template <typename T>
+__global__ void ll_replace_kernel(double* __restrict__ coeff, long long cp,
+                                  const T* __restrict__ ms, long long mp, int hh, int wh,
+                                  double gain) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= hh || j >= wh) return;
+  coeff[(long long)i * cp + j] = mul((double)ms[(long long)i * mp + j], gain);
 }
 
 // ---- rows-only transforms (dwt1d_* is the nrows = 1 case) ------------------
@@ -270,6 +282,27 @@ cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsign
   synth_kernel<<<grid, 256, 0, s>>>(out, pitch, rows, cols, seed, plane, row0, col0);
   return cudaGetLastError();
 }
+
+// fuse_dwt exactly as the reference computes it: float64 forward transform
+// of the PAN plane (its exact operation order), LL <- band * gain, float64
+// inverse, one final cast to the PAN dtype. `ws` = h * w doubles.
+template <typename T>
+cudaError_t launch_fuse_exact(int kind, const T* pan, long long pp, const T* ms, long long mp,
+                              T* out, long long op, int h, int w, double* ws, cudaStream_t s) {
+  dim3 block(32, 8);
+  dim3 grid(((w >> 1) + 31) / 32, ((h >> 1) + 7) / 8);
+  dwt2d_forward_kernel<T, double><<<grid, block, 0, s>>>(kind, pan, pp, ws, w, h, w);
+  ll_replace_kernel<T><<<grid, block, 0, s>>>(ws, w, ms, mp, h >> 1, w >> 1,
+                                              kind == kHaar ? 1.0 : 2.0);
+  dwt2d_inverse_kernel<double, T><<<grid, block, 0, s>>>(kind, ws, w, out, op, h, w);
+  return cudaGetLastError();
+}
+template cudaError_t launch_fuse_exact<float>(int, const float*, long long, const float*,
+                                              long long, float*, long long, int, int, double*,
+                                              cudaStream_t);
+template cudaError_t launch_fuse_exact<double>(int, const double*, long long, const double*,
+                                               long long, double*, long long, int, int, double*,
+                                               cudaStream_t);
 
 template cudaError_t launch_dwt2d<float>(int, bool, const float*, long long, float*, long long,
                                          int, int, cudaStream_t);

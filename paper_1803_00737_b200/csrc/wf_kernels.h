@@ -67,6 +67,12 @@ template <typename T>
 cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long in_pitch, T* out,
                             long long out_pitch, int nrows, int n, cudaStream_t s);
 
+// Reference-exact fuse_dwt: forward (f64, exact order) -> LL <- band*gain ->
+// inverse -> cast; ws holds h*w doubles.
+template <typename T>
+cudaError_t launch_fuse_exact(int kind, const T* pan, long long pp, const T* ms, long long mp,
+                              T* out, long long op, int h, int w, double* ws, cudaStream_t s);
+
 // fusion.py:50-81
 template <typename T, typename To>
 cudaError_t launch_resample(const T* in, long long in_pitch, int in_h, int in_w, To* out,

@@ -384,3 +384,20 @@ def test_host_pipeline_pinned_and_pageable(kname, pinned):
     want = wf.fuse(pan.cuda(), [m.cuda() for m in ms], wf.DwtReplace(KINDS[kname]))
     for o, w_ in zip(out, want):
         assert torch.equal(o, w_.cpu())
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+def test_exact_mode_bit_identical_to_reference(golden_fusion, kname):
+    """fuse(..., exact=True) replays fusion.py:148-150 in float64 with the
+    reference's operation order: every golden output matches bit for bit,
+    float32 and float64 callers alike."""
+    g = golden_fusion
+    for name in _cases(g):
+        if f"{name}/{kname}/out0" not in g:
+            continue
+        pan, bands = g[f"{name}/pan"], _bands(g, name)
+        got = wf.fuse(pan, bands, wf.DwtReplace(KINDS[kname]), exact=True)
+        for b, o in enumerate(got):
+            ref = g[f"{name}/{kname}/out{b}"]
+            assert o.dtype == ref.dtype
+            assert np.array_equal(o, ref), (name, kname, b, _maxabs(o, ref))
