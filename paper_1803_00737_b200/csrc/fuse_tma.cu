@@ -86,11 +86,20 @@ __device__ __forceinline__ uint32_t quantize_u8(float v) {
   return min(__float2uint_rd(__fadd_rn(v, 0.5f)), 255u);
 }
 
+// Same function as quantize_u8 without a float->int conversion: clamp
+// x + 0.5 to [0, 255.5], then 2^23 + c rounded DOWN is exactly
+// 2^23 + floor(c), so the low mantissa byte IS the quantised value and PRMT
+// can pack it straight from the float bits (FADD, 2 FMNMX, FADD.RD).
+__device__ __forceinline__ uint32_t quantize_bits(float v) {
+  const float c = fminf(fmaxf(__fadd_rn(v, 0.5f), 0.0f), 255.5f);
+  return __float_as_uint(__fadd_rd(c, 8388608.0f));
+}
+
 template <typename T, typename Acc>
 __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
   if constexpr (sizeof(T) == 1) {
-    const uint32_t lo = __byte_perm(quantize_u8(o[0]), quantize_u8(o[1]), 0x0040);
-    const uint32_t hi = __byte_perm(quantize_u8(o[2]), quantize_u8(o[3]), 0x0040);
+    const uint32_t lo = __byte_perm(quantize_bits(o[0]), quantize_bits(o[1]), 0x0040);
+    const uint32_t hi = __byte_perm(quantize_bits(o[2]), quantize_bits(o[3]), 0x0040);
     const uint32_t v = __byte_perm(lo, hi, 0x5410);
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
   } else {
@@ -99,7 +108,9 @@ __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
 }
 
 template <typename T, int NB, int NCW>
-__global__ void __launch_bounds__(32 * (NCW + 1))
+// min 4 CTAs/SM: the smem ring (~44 KB) fits 4-5 CTAs; registers must not be
+// the tighter limit (<= 102 per thread at 160 threads)
+__global__ void __launch_bounds__(32 * (NCW + 1), 4)
     fuse_d4_tma_kernel(const FuseArgs<T> a, int S) {
   using Acc = typename TmaTraits<T>::Acc;
   constexpr int HALO = TmaTraits<T>::HALO;
@@ -257,10 +268,26 @@ __global__ void __launch_bounds__(32 * (NCW + 1))
               const Acc v0 = fma(wc, e[1], wp * ep[b][1]);
               const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
               Acc o[4];
-              o[0] = pa[p][0] + fma(h0, v0, h2 * vm);
-              o[1] = pa[p][1] + fma(h1, v0, h3 * vm);
-              o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
-              o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
+              if constexpr (sizeof(Acc) == 4) {
+                // the same four expression trees, issued as packed pairs
+                // (FMUL2/FFMA2/FADD2 round each lane exactly like the scalar ops)
+                const float2 cl = make_float2(h0, h1), ch = make_float2(h2, h3);
+                const float2 o01 = __fadd2_rn(
+                    make_float2(pa[p][0], pa[p][1]),
+                    __ffma2_rn(cl, make_float2(v0, v0), __fmul2_rn(ch, make_float2(vm, vm))));
+                const float2 o23 = __fadd2_rn(
+                    make_float2(pa[p][2], pa[p][3]),
+                    __ffma2_rn(cl, make_float2(v1, v1), __fmul2_rn(ch, make_float2(v0, v0))));
+                o[0] = o01.x;
+                o[1] = o01.y;
+                o[2] = o23.x;
+                o[3] = o23.y;
+              } else {
+                o[0] = pa[p][0] + fma(h0, v0, h2 * vm);
+                o[1] = pa[p][1] + fma(h1, v0, h3 * vm);
+                o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
+                o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
+              }
               T* orow = a.out[0];
 #pragma unroll
               for (int bb = 1; bb < NB; ++bb)
