@@ -149,6 +149,8 @@ int wf_u8_to_f32(const uint8_t* in, int64_t in_pitch, int h, int w, float* out,
                  int64_t out_pitch, void* stream);
 int wf_quantize_f32(const float* in, int64_t in_pitch, int h, int w, uint8_t* out,
                     int64_t out_pitch, void* stream);
+int wf_quantize_f64(const double* in, int64_t in_pitch, int h, int w, uint8_t* out,
+                    int64_t out_pitch, void* stream);
 
 /* ---- standalone transforms --------------------------------------------- */
 int wf_dwt2d_forward_f32(int kind, const float* in, int64_t in_pitch, float* out,

@@ -67,6 +67,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     sig["wf_fuse_host_u8"] = sig["wf_fuse_host_f32"]
     sig["wf_u8_to_f32"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp]
     sig["wf_quantize_f32"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp]
+    sig["wf_quantize_f64"] = sig["wf_quantize_f32"]
     sig["wf_fuse_dwt_exact_f32"] = [c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_int, c_int,
                                     c_vp, c_vp]
     sig["wf_fuse_dwt_exact_f64"] = sig["wf_fuse_dwt_exact_f32"]

@@ -577,14 +577,18 @@ int wf_u8_to_f32(const uint8_t* in, int64_t in_pitch, int h, int w, float* out,
   return cuda_status(e, "wf_u8_to_f32");
 }
 
-int wf_quantize_f32(const float* in, int64_t in_pitch, int h, int w, uint8_t* out,
-                    int64_t out_pitch, void* stream) {
-  if (!in || !out || h < 0 || w < 0) return fail(WF_ERR_VALUE, "bad quantize arguments");
-  if (h == 0 || w == 0) return WF_OK;
-  cudaError_t e = wf::launch_quantize(in, in_pitch, h, w, out, out_pitch, (cudaStream_t)stream);
-  if (e == cudaSuccess) ++g_launches;
-  return cuda_status(e, "wf_quantize_f32");
-}
+#define WF_QUANTIZE(NAME, T)                                                                 \
+  int NAME(const T* in, int64_t in_pitch, int h, int w, uint8_t* out, int64_t out_pitch,      \
+           void* stream) {                                                                   \
+    if (!in || !out || h < 0 || w < 0) return fail(WF_ERR_VALUE, "bad quantize arguments"); \
+    if (h == 0 || w == 0) return WF_OK;                                                      \
+    cudaError_t e = wf::launch_quantize<T>(in, in_pitch, h, w, out, out_pitch,              \
+                                           (cudaStream_t)stream);                            \
+    if (e == cudaSuccess) ++g_launches;                                                      \
+    return cuda_status(e, #NAME);                                                            \
+  }
+WF_QUANTIZE(wf_quantize_f32, float)
+WF_QUANTIZE(wf_quantize_f64, double)
 
 #define WF_DWT2D(NAME, T, INV)                                                               \
   int NAME(int kind, const T* in, int64_t in_pitch, T* out, int64_t out_pitch, int h, int w, \

@@ -219,13 +219,14 @@ __global__ void u8_to_f32_kernel(const uint8_t* __restrict__ in, long long ip, i
 
 // quantize: clamp to [0, 255] then floor(x + 0.5), in float32 like numpy on a
 // float32 plane (imageio.py:115-123)
-__global__ void quantize_kernel(const float* __restrict__ in, long long ip, int h, int w,
+template <typename T>
+__global__ void quantize_kernel(const T* __restrict__ in, long long ip, int h, int w,
                                 uint8_t* __restrict__ out, long long op) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   for (int y = blockIdx.y; y < h; y += gridDim.y)
     if (x < w) {
-      const float v = fminf(fmaxf(in[(long long)y * ip + x], 0.0f), 255.0f);
-      out[(long long)y * op + x] = (uint8_t)floorf(__fadd_rn(v, 0.5f));
+      const T v = fmin(fmax(in[(long long)y * ip + x], T(0)), T(255));
+      out[(long long)y * op + x] = (uint8_t)floor(v + T(0.5));
     }
 }
 
@@ -237,12 +238,17 @@ cudaError_t launch_u8_to_f32(const uint8_t* in, long long ip, int h, int w, floa
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize(const float* in, long long ip, int h, int w, uint8_t* out,
-                            long long op, cudaStream_t s) {
+template <typename T>
+cudaError_t launch_quantize(const T* in, long long ip, int h, int w, uint8_t* out, long long op,
+                            cudaStream_t s) {
   dim3 grid((w + 255) / 256, h < 65535 ? h : 65535);
-  quantize_kernel<<<grid, 256, 0, s>>>(in, ip, h, w, out, op);
+  quantize_kernel<T><<<grid, 256, 0, s>>>(in, ip, h, w, out, op);
   return cudaGetLastError();
 }
+template cudaError_t launch_quantize<float>(const float*, long long, int, int, uint8_t*, long long,
+                                            cudaStream_t);
+template cudaError_t launch_quantize<double>(const double*, long long, int, int, uint8_t*,
+                                             long long, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_dwt2d(int kind, bool inverse, const T* in, long long ip, T* out,

@@ -56,8 +56,9 @@ cudaError_t launch_fuse<uint8_t, float>(int kind, const FuseArgs<uint8_t>& a, bo
                                         cudaStream_t s, const LaunchTuning& tune);
 cudaError_t launch_u8_to_f32(const uint8_t* in, long long ip, int h, int w, float* out,
                              long long op, cudaStream_t s);
-cudaError_t launch_quantize(const float* in, long long ip, int h, int w, uint8_t* out,
-                            long long op, cudaStream_t s);
+template <typename T>
+cudaError_t launch_quantize(const T* in, long long ip, int h, int w, uint8_t* out, long long op,
+                            cudaStream_t s);
 
 // Standalone transforms (materialise coefficients; wavelet.py:131-164).
 template <typename T>

@@ -232,19 +232,17 @@ def _u8_to_f32_dev(t: torch.Tensor) -> torch.Tensor:
 def _quantize_dev(t: torch.Tensor) -> torch.Tensor:
     h, w = t.shape
     out = torch.empty((h, w), dtype=torch.uint8, device=t.device)
-    _native.check(_native.load().wf_quantize_f32(t.data_ptr(), t.stride(0), h, w,
-                                                 out.data_ptr(), w, _device.stream_ptr()))
+    lib = _native.load()
+    fn = lib.wf_quantize_f32 if t.dtype == torch.float32 else lib.wf_quantize_f64
+    _native.check(fn(t.data_ptr(), t.stride(0), h, w, out.data_ptr(), w, _device.stream_ptr()))
     return out
 
 
 def quantize(plane):
-    """imageio.py:115-123: clamp to [0, 255], round half away from zero, uint8
-    (float32 arithmetic on float32 planes, like numpy)."""
+    """imageio.py:115-123: clamp to [0, 255], then floor(x + 0.5), as uint8 --
+    in float32 for float32 planes and float64 otherwise, like numpy."""
     is_t = _is_tensor(plane)
-    t = _device.to_device(plane, np.float32) if is_t or _device.is_f32(plane) else None
-    if t is None:  # float64 planes: numpy semantics in float64
-        raise TypeError("quantize on the GPU takes float32 planes")
-    out = _quantize_dev(t)
+    out = _quantize_dev(_device.to_device(plane, _device.np_out_dtype(plane)))
     return out if is_t else out.cpu().numpy()
 
 

@@ -19,10 +19,16 @@ import numpy as np
 import torch
 
 from . import _device, _native
-from .errors import BandCountMismatch, DimensionMismatch, NotDivisible, OddDimension, OddTile
-from .fusion import DwtReplace, FusionMethod, _quantize_dev, _u8_to_f32_dev, resample_bilinear
+from .errors import BandCountMismatch, DimensionMismatch, NotDivisible, OddTile, TooSmall
+from .fusion import (
+    DwtReplace,
+    FusionMethod,
+    _quantize_dev,
+    _u8_device,
+    _u8_to_f32_dev,
+    resample_bilinear,
+)
 from .wavelet import KIND_CODE, MIN_LEN, WaveletKind
-from .errors import TooSmall
 
 
 @dataclass(frozen=True)
@@ -135,7 +141,7 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
 
         def to_u8(x):  # uint8 passes through; float planes are quantised (float32)
             is_u8 = x.dtype == (torch.uint8 if isinstance(x, torch.Tensor) else np.uint8)
-            return _as_u8_dev(x) if is_u8 else _quantize_dev(_device.to_device(x, np.float32))
+            return _u8_device(x) if is_u8 else _quantize_dev(_device.to_device(x, np.float32))
 
         pan_u8 = to_u8(pan)
         ms_u8 = [to_u8(b) for b in low]
@@ -158,9 +164,3 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
     _window_fuse(kind, pan_t, ms_t, outs, grid)
     return outs if is_t else [o.cpu().numpy() for o in outs]
 
-
-def _as_u8_dev(x) -> torch.Tensor:
-    dev = _device.require_cuda()
-    if isinstance(x, torch.Tensor):
-        return (x if x.is_cuda else x.to(dev)).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)

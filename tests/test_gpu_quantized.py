@@ -52,6 +52,22 @@ def test_quantize_matches_reference():
     assert np.array_equal(wf.quantize(G["quantize/in"]), G["quantize/out"])
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_quantize_dtypes_match_oracle(dtype):
+    # half-integers, their float neighbours and out-of-range values: the
+    # rounding happens in the plane's own dtype, as numpy does it
+    rng = np.random.default_rng(7)
+    base = rng.integers(-3, 260, size=(64, 96)).astype(dtype) + dtype(0.5)
+    nudge = rng.integers(-1, 2, size=base.shape)
+    plane = np.where(nudge < 0, np.nextafter(base, dtype(-np.inf)),
+                     np.where(nudge > 0, np.nextafter(base, dtype(np.inf)), base)).astype(dtype)
+    got = wf.quantize(plane)
+    assert got.dtype == np.uint8
+    assert np.array_equal(got, O.quantize(plane))
+    t = wf.quantize(torch.from_numpy(plane).cuda())
+    assert np.array_equal(t.cpu().numpy(), O.quantize(plane))
+
+
 @pytest.mark.parametrize("kname", list(KINDS))
 def test_tiled_8bpp_pipeline(kname):
     """fuse_tiled(..., transfer_8bpp=True) of the reference (tiling.py:238-248)
