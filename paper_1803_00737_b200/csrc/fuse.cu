@@ -402,8 +402,21 @@ cudaError_t launch_fuse(int kind, const FuseArgs<T>& a, bool vec, bool tma, cuda
 // PAN/MS in, quantised uint8 out (imageio.py:115-123 fused into the store).
 // With integer inputs every intermediate is a multiple of 1/4, exact in
 // float32, so the result is bit-identical to quantize(fuse_dwt(...)) of the
-// float64 reference. A thread owns 16 PAN columns x 2 rows (uint4 I/O).
+// float64 reference:
+//   quantize(pan + ms - mean2x2) = clamp(x, 0, 1023) >> 2,
+//   x = 4*pan + 4*ms + 2 - (sum of the 2x2 cell)     (x in [-1018, 2042])
+// (clamp-then-shift equals the floor-then-clamp of imageio.py:115-123 on the
+// exact value). The arithmetic runs two pixels per register in signed 16-bit
+// lanes: one VIADDMNMX.S16x2.RELU adds the band term and clamps both lanes,
+// so a pixel costs ~1.5 integer ops per band instead of ~5 (the scalar form
+// was ALU-pipe bound). A thread owns 16 PAN columns x 2 rows (uint4 I/O).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t mask) {
+  uint32_t r;  // (a & mask) | (b & ~mask)
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(mask));
+  return r;
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kHaarThreads)
     fuse_haar_u8_kernel(const FuseArgs<uint8_t> a) {
@@ -424,25 +437,21 @@ __global__ void __launch_bounds__(kHaarThreads)
     asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
         : "=r"(w1.x), "=r"(w1.y), "=r"(w1.z), "=r"(w1.w)
         : "l"(r0 + a.pan_pitch));
-    // Integer form of the same arithmetic: every value is a multiple of 1/4,
-    // so with P = 4*pan, C = 2 - (sum of the 2x2 cell) and M = 4*ms,
-    //   quantize(pan + ms - mean2x2) = clamp((P + M + C) >> 2, 0, 255)
-    // (arithmetic shift = floor; identical to floor(clamp(v) + 0.5) of
-    // imageio.py:115-123 on the exact float value).
     const uint32_t p0w[4] = {w0.x, w0.y, w0.z, w0.w}, p1w[4] = {w1.x, w1.y, w1.z, w1.w};
-    int q0[16], q1[16];
+    // Per 4-column word d (cells 2d, 2d+1), lanes (lo, hi):
+    //   ev[r][d] = 4*pan + 2 - cell sum at columns (4d, 4d+2) of row r,
+    //   od[r][d] = the same at columns (4d+1, 4d+3)
+    uint32_t ev[2][4], od[2][4];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      q0[k] = (int)((p0w[k >> 2] >> (8 * (k & 3))) & 0xffu);
-      q1[k] = (int)((p1w[k >> 2] >> (8 * (k & 3))) & 0xffu);
-    }
-    int cell[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) cell[k] = 2 - (q0[2 * k] + q0[2 * k + 1] + q1[2 * k] + q1[2 * k + 1]);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      q0[k] *= 4;
-      q1[k] *= 4;
+    for (int d = 0; d < 4; ++d) {
+      const uint32_t e0 = __byte_perm(p0w[d], 0u, 0x4240), o0 = __byte_perm(p0w[d], 0u, 0x4341);
+      const uint32_t e1 = __byte_perm(p1w[d], 0u, 0x4240), o1 = __byte_perm(p1w[d], 0u, 0x4341);
+      const uint32_t cell = e0 + o0 + e1 + o1;            // lanes <= 1020: no carries
+      const uint32_t c2 = __vsub2(0x00020002u, cell);     // 2 - sum, signed lanes
+      ev[0][d] = __vadd2(e0 << 2, c2);
+      od[0][d] = __vadd2(o0 << 2, c2);
+      ev[1][d] = __vadd2(e1 << 2, c2);
+      od[1][d] = __vadd2(o1 << 2, c2);
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -450,31 +459,25 @@ __global__ void __launch_bounds__(kHaarThreads)
       asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
           : "=r"(mw.x), "=r"(mw.y)
           : "l"(a.ms[b] + (long long)i * a.ms_pitch + (c >> 1)));
-      const uint32_t mwv[2] = {mw.x, mw.y};
-      uint32_t r0v[16], r1v[16];
+      uint32_t o[2][4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = 4 * (int)((mwv[k >> 2] >> (8 * (k & 3))) & 0xffu) + cell[k];
+      for (int d = 0; d < 4; ++d) {
+        // 4*ms of cells (2d, 2d+1) in lanes (lo, hi)
+        const uint32_t m4 = __byte_perm(d < 2 ? mw.x : mw.y, 0u, (d & 1) ? 0x4342 : 0x4140) << 2;
 #pragma unroll
-        for (int x = 2 * k; x < 2 * k + 2; ++x) {
-          r0v[x] = (uint32_t)min(max((q0[x] + t) >> 2, 0), 255);
-          r1v[x] = (uint32_t)min(max((q1[x] + t) >> 2, 0), 255);
+        for (int r = 0; r < 2; ++r) {
+          const uint32_t ye = __viaddmin_s16x2_relu(ev[r][d], m4, 0x03FF03FFu);
+          const uint32_t yo = __viaddmin_s16x2_relu(od[r][d], m4, 0x03FF03FFu);
+          // bytes 0,2 <- ye >> 2 (columns 4d, 4d+2); bytes 1,3 <- yo >> 2
+          o[r][d] = lop3_sel(ye >> 2, yo << 6, 0x00FF00FFu);
         }
       }
-      uint32_t o0[4], o1[4];
-#pragma unroll
-      for (int wd = 0; wd < 4; ++wd) {
-        o0[wd] = __byte_perm(__byte_perm(r0v[4 * wd], r0v[4 * wd + 1], 0x0040),
-                             __byte_perm(r0v[4 * wd + 2], r0v[4 * wd + 3], 0x0040), 0x5410);
-        o1[wd] = __byte_perm(__byte_perm(r1v[4 * wd], r1v[4 * wd + 1], 0x0040),
-                             __byte_perm(r1v[4 * wd + 2], r1v[4 * wd + 3], 0x0040), 0x5410);
-      }
       uint8_t* w = a.out[b] + (long long)(2 * i) * a.out_pitch + c;
-      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(w), "r"(o0[0]), "r"(o0[1]),
-                   "r"(o0[2]), "r"(o0[3])
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(w), "r"(o[0][0]), "r"(o[0][1]),
+                   "r"(o[0][2]), "r"(o[0][3])
                    : "memory");
       asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(w + a.out_pitch),
-                   "r"(o1[0]), "r"(o1[1]), "r"(o1[2]), "r"(o1[3])
+                   "r"(o[1][0]), "r"(o[1][1]), "r"(o[1][2]), "r"(o[1][3])
                    : "memory");
     }
   }

@@ -30,15 +30,20 @@
 
 namespace wf {
 
+// MIN_CTAS: the 4-byte and 1-byte rings (~44 KB) fit 4-5 CTAs per SM, so
+// registers must not be the tighter limit (<= 96 per thread at 160 threads);
+// float64 state needs twice the registers, and 2 CTAs/SM keep it unspilled.
 template <typename T>
 struct TmaTraits {
   using Acc = T;
   static constexpr int HALO = 16 / (int)sizeof(T) >= 4 ? 16 / (int)sizeof(T) : 4;
+  static constexpr int MIN_CTAS = sizeof(T) == 8 ? 2 : 4;
 };
 template <>
 struct TmaTraits<uint8_t> {
   using Acc = float;
   static constexpr int HALO = 16;  // bulk-copy pieces are multiples of 16 bytes
+  static constexpr int MIN_CTAS = 4;
 };
 
 template <typename Acc>
@@ -78,29 +83,28 @@ __device__ __forceinline__ void lds2(const T* p, Acc& x, Acc& y) {
   }
 }
 
-// imageio.py:115-123 quantize (clamp to [0, 255], then floor(x + 0.5) in
-// float32). For |x| < 2^22, x + 0.5 is exact, so clamping after the floor is
-// the same function: FADD, F2I.U32 with round-down (saturates negatives to
-// 0), IMNMX.
-__device__ __forceinline__ uint32_t quantize_u8(float v) {
-  return min(__float2uint_rd(__fadd_rn(v, 0.5f)), 255u);
+// imageio.py:115-123 quantize of two values: clamp(x + 0.5, 0, 255), floor,
+// uint8 -- in float32, like numpy on a float32 plane -- with no float->int
+// conversion. c = x + 0.5 (FADD2) is clamped to [0, 255.5] on its bit pattern
+// (VIMNMX.RELU: max(min(bits, bits(255.5)), 0) orders finite floats like the
+// float clamp, and maps -0 and negatives to +0); then 2^23 + c rounded DOWN
+// (FADD2.RM) is exactly 2^23 + floor(c), so the low mantissa byte is the
+// quantised value. Result: the two bytes in bits 0-15.
+__device__ __forceinline__ uint32_t quantize_pair(float2 v) {
+  const float2 c = __fadd2_rn(v, make_float2(0.5f, 0.5f));
+  const int kMax = 0x437F8000;  // 255.5f
+  const float2 cl = make_float2(__int_as_float(__vimin_s32_relu(__float_as_int(c.x), kMax)),
+                                __int_as_float(__vimin_s32_relu(__float_as_int(c.y), kMax)));
+  const float2 r = __fadd2_rd(cl, make_float2(8388608.0f, 8388608.0f));
+  return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040);
 }
 
-// Same function as quantize_u8 without a float->int conversion: clamp
-// x + 0.5 to [0, 255.5], then 2^23 + c rounded DOWN is exactly
-// 2^23 + floor(c), so the low mantissa byte IS the quantised value and PRMT
-// can pack it straight from the float bits (FADD, 2 FMNMX, FADD.RD).
-__device__ __forceinline__ uint32_t quantize_bits(float v) {
-  const float c = fminf(fmaxf(__fadd_rn(v, 0.5f), 0.0f), 255.5f);
-  return __float_as_uint(__fadd_rd(c, 8388608.0f));
-}
-
+// four consecutive outputs (two pairs) to row-major storage
 template <typename T, typename Acc>
 __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
   if constexpr (sizeof(T) == 1) {
-    const uint32_t lo = __byte_perm(quantize_bits(o[0]), quantize_bits(o[1]), 0x0040);
-    const uint32_t hi = __byte_perm(quantize_bits(o[2]), quantize_bits(o[3]), 0x0040);
-    const uint32_t v = __byte_perm(lo, hi, 0x5410);
+    const uint32_t v = __byte_perm(quantize_pair(make_float2(o[0], o[1])),
+                                   quantize_pair(make_float2(o[2], o[3])), 0x5410);
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
   } else {
     store4_vec<Acc>(p, o);
@@ -108,9 +112,7 @@ __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
 }
 
 template <typename T, int NB, int NCW>
-// min 4 CTAs/SM: the smem ring (~44 KB) fits 4-5 CTAs; registers must not be
-// the tighter limit (<= 102 per thread at 160 threads)
-__global__ void __launch_bounds__(32 * (NCW + 1), 4)
+__global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
     fuse_d4_tma_kernel(const FuseArgs<T> a, int S) {
   using Acc = typename TmaTraits<T>::Acc;
   constexpr int HALO = TmaTraits<T>::HALO;
@@ -223,17 +225,14 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 4)
       lds2<T, Acc>(pr + 2, v[q][4], v[q][5]);
       lds2<T, Acc>(pr + 4, v[q][6], v[q][7]);
     }
-    Acc m[NB][3];
-    if (n >= 1) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const T* mr = slot + 2 * PROW + b * MROW + HALO + (rel >> 1);
-        m[b][0] = (Acc)mr[-1];
-        lds2<T, Acc>(mr, m[b][1], m[b][2]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[s]);
+    // MS band b at half-cols j-1, j, j+1, read from the slot as each band is
+    // fused (the slot is released after the band loop), so the NB x 3 values
+    // never all sit in registers
+    auto ms3 = [&](int b, Acc (&m3)[3]) {
+      const T* mr = slot + 2 * PROW + b * MROW + HALO + (rel >> 1);
+      m3[0] = (Acc)mr[-1];
+      lds2<T, Acc>(mr, m3[1], m3[2]);
+    };
 
     Acc rn[2][3];
 #pragma unroll
@@ -249,17 +248,26 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 4)
         ll[jj] = dot4t(h0, h1, h2, h3, rprev[0][jj], rprev[1][jj], rn[0][jj], rn[1][jj]);
       if (n == 1) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+        for (int b = 0; b < NB; ++b) {
+          Acc m3[3];
+          ms3(b, m3);
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = m[b][jj] + m[b][jj] - ll[jj];
+          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = m3[jj] + m3[jj] - ll[jj];
+        }
       } else {
         const int i = i0 + n - 2;
+        const long long off0 = (long long)(2 * i) * a.out_pitch + c;  // row 2i, this thread's column
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          Acc e[3];
+          Acc m3[3], e[3];
+          ms3(b, m3);
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) e[jj] = m[b][jj] + m[b][jj] - ll[jj];
+          for (int jj = 0; jj < 3; ++jj) e[jj] = m3[jj] + m3[jj] - ll[jj];
           if (valid) {
+            T* orow = a.out[0];
+#pragma unroll
+            for (int bb = 1; bb < NB; ++bb)
+              if (b == bb) orow = a.out[bb];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
               const Acc wp = p == 0 ? h2 : h3;
@@ -288,11 +296,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 4)
                 o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
                 o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
               }
-              T* orow = a.out[0];
-#pragma unroll
-              for (int bb = 1; bb < NB; ++bb)
-                if (b == bb) orow = a.out[bb];
-              store4_out<T, Acc>(orow + (long long)(2 * i + p) * a.out_pitch + c, o);
+              store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
             }
           }
 #pragma unroll
@@ -308,6 +312,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 4)
     for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int jj = 0; jj < 3; ++jj) rprev[q][jj] = rn[q][jj];
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
   }
 }
 
@@ -336,7 +342,7 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
   // runs amortise the 2-pair prologue when there is little per-pair work
   // (tools/sweep_d4.py on the Landsat scene: B >= 4 -> 4, B = 2..3 -> 8, B = 1 -> 32)
   int P = tune.d4_pairs > 0 ? tune.d4_pairs
-                            : (sizeof(T) == 1 ? 16 : (NB == 1 ? 32 : (NB <= 3 ? 8 : 4)));
+                            : (sizeof(T) == 1 ? 32 : (NB == 1 ? 32 : (NB <= 3 ? 8 : 4)));
   if (P > npairs) P = npairs;
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;

@@ -93,6 +93,27 @@ def test_tiled_8bpp_pipeline(kname):
             assert _flips(out[b], ref) <= 4
 
 
+def test_u8_haar_saturating_values():
+    """The 16-bit-lane Haar kernel at the clamp edges: planes drawn mostly from
+    {0, 1, 2, 253, 254, 255} drive every lane to both saturation bounds and
+    to the round-down boundaries; bit-exact against the oracle."""
+    rng = np.random.default_rng(11)
+    H, W, B = 512, 1024, 8
+    edge = np.array([0, 1, 2, 3, 252, 253, 254, 255], np.uint8)
+
+    def plane(shape):
+        x = rng.integers(0, 256, shape, dtype=np.uint8)
+        pick = rng.random(shape) < 0.8
+        return np.where(pick, edge[rng.integers(0, edge.size, shape)], x).astype(np.uint8)
+
+    pan = plane((H, W))
+    ms = [plane((H // 2, W // 2)) for _ in range(B)]
+    got = wf.fuse_quantized(pan, ms, wf.DwtReplace(KINDS["haar"]))
+    ref = O.fuse_quantized(pan, ms, "haar")
+    for g, r in zip(got, ref):
+        assert np.array_equal(g, r)
+
+
 @pytest.mark.parametrize("kname", list(KINDS))
 def test_large_u8_scene_vs_oracle(kname):
     """2048 x 4096, 6 bands through the 8 bpp kernels (device tensors and the

@@ -1,4 +1,5 @@
-"""Warm-up + profiled launches of the 8 bpp D4 kernel on the Landsat scene."""
+"""Warm-up + profiled launches of an 8 bpp fusion kernel on the Landsat scene
+(argv[1]: 1 = Haar, 2 = D4; default D4)."""
 import os
 import sys
 
@@ -17,7 +18,8 @@ out = [torch.empty((H, W), dtype=torch.uint8, device="cuda") for _ in ms]
 lib = _native.load()
 mp = _native.ptr_array([m.data_ptr() for m in ms])
 op = _native.ptr_array([o.data_ptr() for o in out])
+KIND = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 for _ in range(2):
-    _native.check(lib.wf_fuse_bands_u8(2, pan.data_ptr(), W, mp, W // 2, op, W, B, H, W, None))
+    _native.check(lib.wf_fuse_bands_u8(KIND, pan.data_ptr(), W, mp, W // 2, op, W, B, H, W, None))
 torch.cuda.synchronize()
 print("profile_u8 ok")
