@@ -39,11 +39,14 @@ struct TmaTraits {
   static constexpr int HALO = 16 / (int)sizeof(T) >= 4 ? 16 / (int)sizeof(T) : 4;
   static constexpr int MIN_CTAS = sizeof(T) == 8 ? 2 : 4;
 };
+#ifndef WF_U8_MIN_CTAS  // build-time experiment knob; 2, 3, 5, 6 all measured slower
+#define WF_U8_MIN_CTAS 4
+#endif
 template <>
 struct TmaTraits<uint8_t> {
   using Acc = float;
   static constexpr int HALO = 16;  // bulk-copy pieces are multiples of 16 bytes
-  static constexpr int MIN_CTAS = 4;
+  static constexpr int MIN_CTAS = WF_U8_MIN_CTAS;
 };
 
 template <typename Acc>
@@ -83,28 +86,31 @@ __device__ __forceinline__ void lds2(const T* p, Acc& x, Acc& y) {
   }
 }
 
-// imageio.py:115-123 quantize of two values: clamp(x + 0.5, 0, 255), floor,
-// uint8 -- in float32, like numpy on a float32 plane -- with no float->int
-// conversion. c = x + 0.5 (FADD2) is clamped to [0, 255.5] on its bit pattern
-// (VIMNMX.RELU: max(min(bits, bits(255.5)), 0) orders finite floats like the
-// float clamp, and maps -0 and negatives to +0); then 2^23 + c rounded DOWN
-// (FADD2.RM) is exactly 2^23 + floor(c), so the low mantissa byte is the
-// quantised value. Result: the two bytes in bits 0-15.
-__device__ __forceinline__ uint32_t quantize_pair(float2 v) {
+// imageio.py:115-123 quantize -- clamp(x + 0.5, 0, 255), floor, uint8, in
+// float32 like numpy on a float32 plane -- of four fused values, packed into
+// one word with no float->int conversion:
+//   c = x + 0.5                      FADD2 (the same rounding as numpy's)
+//   r = 2^23 + 2^15 + c, rounded DOWN FADD2.RM: exactly 2^23 + 2^15 + floor(c)
+//                                     while |c| < 2^15, so r's low 16 bits
+//                                     are floor(c) + 2^15
+//   lanes <- low halves of two r      PRMT
+//   clamp(lane - 2^15, 0, 255)        VIADDMNMX.S16x2.RELU (both lanes)
+//   bytes <- the four lane bytes      PRMT
+// An 8 bpp fused value is pan + S_LL(2 ms - LL(pan)) with |value| < 4000,
+// far inside the 2^15 window.
+__device__ __forceinline__ uint32_t quantize_lanes(float2 v) {
   const float2 c = __fadd2_rn(v, make_float2(0.5f, 0.5f));
-  const int kMax = 0x437F8000;  // 255.5f
-  const float2 cl = make_float2(__int_as_float(__vimin_s32_relu(__float_as_int(c.x), kMax)),
-                                __int_as_float(__vimin_s32_relu(__float_as_int(c.y), kMax)));
-  const float2 r = __fadd2_rd(cl, make_float2(8388608.0f, 8388608.0f));
-  return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040);
+  const float2 r = __fadd2_rd(c, make_float2(8421376.0f, 8421376.0f));  // 2^23 + 2^15
+  const uint32_t l = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x5410);
+  return __viaddmin_s16x2_relu(l, 0x80008000u, 0x00FF00FFu);
 }
 
-// four consecutive outputs (two pairs) to row-major storage
+// four consecutive outputs to row-major storage
 template <typename T, typename Acc>
 __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
   if constexpr (sizeof(T) == 1) {
-    const uint32_t v = __byte_perm(quantize_pair(make_float2(o[0], o[1])),
-                                   quantize_pair(make_float2(o[2], o[3])), 0x5410);
+    const uint32_t v = __byte_perm(quantize_lanes(make_float2(o[0], o[1])),
+                                   quantize_lanes(make_float2(o[2], o[3])), 0x6420);
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
   } else {
     store4_vec<Acc>(p, o);
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
           Acc m3[3];
           ms3(b, m3);
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = m3[jj] + m3[jj] - ll[jj];
+          for (int jj = 0; jj < 3; ++jj) ep[b][jj] = fma(Acc(2), m3[jj], -ll[jj]);
         }
       } else {
         const int i = i0 + n - 2;
@@ -262,41 +268,49 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
           Acc m3[3], e[3];
           ms3(b, m3);
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) e[jj] = m3[jj] + m3[jj] - ll[jj];
+          // E = 2*ms - LL: 2*ms is exact, so one rounding like (ms + ms) - LL
+          for (int jj = 0; jj < 3; ++jj) e[jj] = fma(Acc(2), m3[jj], -ll[jj]);
           if (valid) {
             T* orow = a.out[0];
 #pragma unroll
             for (int bb = 1; bb < NB; ++bb)
               if (b == bb) orow = a.out[bb];
+            if constexpr (sizeof(Acc) == 4) {
+              // the scalar expression trees of the branch below, issued as
+              // packed pairs -- first over the two output rows, then over
+              // column pairs (FMUL2/FFMA2/FADD2 round each lane exactly like
+              // the scalar ops)
+              const float2 wc = make_float2(h0, h1), wp = make_float2(h2, h3);
+              const float2 vm = __ffma2_rn(wc, make_float2(e[0], e[0]),
+                                           __fmul2_rn(wp, make_float2(ep[b][0], ep[b][0])));
+              const float2 v0 = __ffma2_rn(wc, make_float2(e[1], e[1]),
+                                           __fmul2_rn(wp, make_float2(ep[b][1], ep[b][1])));
+              const float2 v1 = __ffma2_rn(wc, make_float2(e[2], e[2]),
+                                           __fmul2_rn(wp, make_float2(ep[b][2], ep[b][2])));
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
-              const Acc wp = p == 0 ? h2 : h3;
-              const Acc wc = p == 0 ? h0 : h1;
-              const Acc vm = fma(wc, e[0], wp * ep[b][0]);
-              const Acc v0 = fma(wc, e[1], wp * ep[b][1]);
-              const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
-              Acc o[4];
-              if constexpr (sizeof(Acc) == 4) {
-                // the same four expression trees, issued as packed pairs
-                // (FMUL2/FFMA2/FADD2 round each lane exactly like the scalar ops)
-                const float2 cl = make_float2(h0, h1), ch = make_float2(h2, h3);
+              for (int p = 0; p < 2; ++p) {
+                const float vmp = p ? vm.y : vm.x, v0p = p ? v0.y : v0.x, v1p = p ? v1.y : v1.x;
                 const float2 o01 = __fadd2_rn(
                     make_float2(pa[p][0], pa[p][1]),
-                    __ffma2_rn(cl, make_float2(v0, v0), __fmul2_rn(ch, make_float2(vm, vm))));
+                    __ffma2_rn(wc, make_float2(v0p, v0p), __fmul2_rn(wp, make_float2(vmp, vmp))));
                 const float2 o23 = __fadd2_rn(
                     make_float2(pa[p][2], pa[p][3]),
-                    __ffma2_rn(cl, make_float2(v1, v1), __fmul2_rn(ch, make_float2(v0, v0))));
-                o[0] = o01.x;
-                o[1] = o01.y;
-                o[2] = o23.x;
-                o[3] = o23.y;
-              } else {
-                o[0] = pa[p][0] + fma(h0, v0, h2 * vm);
-                o[1] = pa[p][1] + fma(h1, v0, h3 * vm);
-                o[2] = pa[p][2] + fma(h0, v1, h2 * v0);
-                o[3] = pa[p][3] + fma(h1, v1, h3 * v0);
+                    __ffma2_rn(wc, make_float2(v1p, v1p), __fmul2_rn(wp, make_float2(v0p, v0p))));
+                const Acc o[4] = {o01.x, o01.y, o23.x, o23.y};
+                store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
               }
-              store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+            } else {
+#pragma unroll
+              for (int p = 0; p < 2; ++p) {
+                const Acc wp = p == 0 ? h2 : h3;
+                const Acc wc = p == 0 ? h0 : h1;
+                const Acc vm = fma(wc, e[0], wp * ep[b][0]);
+                const Acc v0 = fma(wc, e[1], wp * ep[b][1]);
+                const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
+                const Acc o[4] = {pa[p][0] + fma(h0, v0, h2 * vm), pa[p][1] + fma(h1, v0, h3 * vm),
+                                  pa[p][2] + fma(h0, v1, h2 * v0), pa[p][3] + fma(h1, v1, h3 * v0)};
+                store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+              }
             }
           }
 #pragma unroll
