@@ -25,6 +25,9 @@
  *   wf_q_index             metrics.py:45-83    q_index(a, b)
  *   wf_ergas_band          metrics.py:94-119   ergas() per band
  *   wf_quality_scene_f32   metrics.py:178-199  qnr() in one pass over the scene
+ *   wf_raster_to_plane_*   imageio.py:104-112 to_plane + tiling.py:285-293 pad_edge
+ *   wf_pad_edge_*          tiling.py:285-293   pad_edge(plane, out_w, out_h)
+ *   wf_planes_to_raster_*  cli.py:135-164      quantize + crop + interleave (PGM/PPM payload)
  *
  * Conventions
  *  - All array arguments of the device entry points are DEVICE pointers;
@@ -68,7 +71,8 @@ enum {
   WF_ERR_BAND_COUNT = 6,         /* errors.BandCountMismatch                   */
   WF_ERR_ODD_LENGTH = 7,         /* errors.OddLength                           */
   WF_ERR_TOO_SHORT = 8,          /* errors.TooShort                            */
-  WF_ERR_NOT_DIVISIBLE = 9       /* errors.NotDivisible                        */
+  WF_ERR_NOT_DIVISIBLE = 9,      /* errors.NotDivisible                        */
+  WF_ERR_CHANNEL = 10            /* errors.ChannelOutOfRange                   */
 };
 
 #define WF_MAX_BANDS_PER_LAUNCH 8
@@ -151,6 +155,33 @@ int wf_quantize_f32(const float* in, int64_t in_pitch, int h, int w, uint8_t* ou
                     int64_t out_pitch, void* stream);
 int wf_quantize_f64(const double* in, int64_t in_pitch, int h, int w, uint8_t* out,
                     int64_t out_pitch, void* stream);
+
+/* ---- PNM front end (cli.py:113-165) -------------
+ * The per-pixel half of the CLI path; PGM/PPM header parsing stays on the
+ * host. `raster` is the row-major, channel-interleaved uint8 payload
+ * (h x w x channels) of imageio.py:46-87.
+ * wf_raster_to_plane_*: imageio.py:104-112 to_plane(raster, channel) fused
+ *   with tiling.py:285-293 pad_edge to out_h x out_w (>= h x w; the last row
+ *   and column are replicated). channel outside [0, channels) ->
+ *   WF_ERR_CHANNEL; out dims below h x w -> WF_ERR_VALUE. */
+int wf_raster_to_plane_f32(const uint8_t* raster, int h, int w, int channels, int channel,
+                           float* out, int64_t out_pitch, int out_h, int out_w, void* stream);
+int wf_raster_to_plane_f64(const uint8_t* raster, int h, int w, int channels, int channel,
+                           double* out, int64_t out_pitch, int out_h, int out_w, void* stream);
+/* tiling.py:285-293 pad_edge(plane, out_w, out_h) of a float plane. */
+int wf_pad_edge_f32(const float* in, int64_t in_pitch, int h, int w, float* out,
+                    int64_t out_pitch, int out_h, int out_w, void* stream);
+int wf_pad_edge_f64(const double* in, int64_t in_pitch, int h, int w, double* out,
+                    int64_t out_pitch, int out_h, int out_w, void* stream);
+/* cli.py:135-164: quantize (imageio.py:115-123, in the planes' dtype) of the
+ * top-left h x w window (the crop b[:h, :w]) of `nplanes` (1..8) planes with
+ * a common pitch, interleaved into raster (h x w x nplanes): the PGM payload
+ * for one plane, the PPM one (np.stack(bands, axis=-1)) for three.
+ * `planes` is a host array of device pointers. */
+int wf_planes_to_raster_f32(const float* const* planes, int nplanes, int64_t pitch, int h, int w,
+                            uint8_t* raster, void* stream);
+int wf_planes_to_raster_f64(const double* const* planes, int nplanes, int64_t pitch, int h, int w,
+                            uint8_t* raster, void* stream);
 
 /* ---- standalone transforms --------------------------------------------- */
 int wf_dwt2d_forward_f32(int kind, const float* in, int64_t in_pitch, float* out,

@@ -10,9 +10,11 @@ is no CPU fallback.
 
 from .errors import (
     BandCountMismatch,
+    ChannelOutOfRange,
     CudaError,
     DimensionMismatch,
     FusionError,
+    MalformedHeader,
     NotDivisible,
     OddDimension,
     OddLength,
@@ -20,6 +22,8 @@ from .errors import (
     TooFewBands,
     TooShort,
     TooSmall,
+    Truncated,
+    UnsupportedFormat,
     ZeroBandMean,
 )
 from .fusion import (
@@ -34,7 +38,8 @@ from .fusion import (
     resample_bilinear,
 )
 from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, q_index, qnr
-from .tiling import TileGrid, fuse_tiled, padded_dims, plan_grid
+from .pnm import PnmRaster, fuse_pnm, read_pnm, to_plane, write_pnm
+from .tiling import TileGrid, fuse_tiled, pad_edge, pad_inputs, padded_dims, plan_grid
 from .wavelet import (
     FilterBank,
     WaveletKind,
@@ -49,21 +54,26 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BandCountMismatch",
+    "ChannelOutOfRange",
     "CudaError",
     "DimensionMismatch",
     "DwtReplace",
     "FilterBank",
     "FusionError",
     "FusionMethod",
+    "MalformedHeader",
     "NotDivisible",
     "OddDimension",
     "OddLength",
     "OddTile",
+    "PnmRaster",
     "QualityReport",
     "TileGrid",
     "TooFewBands",
     "TooShort",
     "TooSmall",
+    "Truncated",
+    "UnsupportedFormat",
     "WaveletKind",
     "ZeroBandMean",
     "__version__",
@@ -78,14 +88,20 @@ __all__ = [
     "ergas",
     "fuse",
     "fuse_dwt",
+    "fuse_pnm",
     "fuse_quantized",
     "fuse_tile_quantized",
     "fuse_tiled",
     "method_from_name",
+    "pad_edge",
+    "pad_inputs",
     "padded_dims",
     "plan_grid",
     "q_index",
     "qnr",
     "quantize",
+    "read_pnm",
     "resample_bilinear",
+    "to_plane",
+    "write_pnm",
 ]

@@ -30,6 +30,7 @@ _ERR = {
     7: errors.OddLength,
     8: errors.TooShort,
     9: errors.NotDivisible,
+    10: errors.ChannelOutOfRange,
 }
 
 _lock = threading.Lock()
@@ -71,6 +72,11 @@ def _declare(lib: ctypes.CDLL) -> None:
     sig["wf_fuse_dwt_exact_f32"] = [c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_int, c_int,
                                     c_vp, c_vp]
     sig["wf_fuse_dwt_exact_f64"] = sig["wf_fuse_dwt_exact_f32"]
+    for t in ("f32", "f64"):
+        sig[f"wf_raster_to_plane_{t}"] = [c_vp, c_int, c_int, c_int, c_int, c_vp, c_i64, c_int,
+                                          c_int, c_vp]
+        sig[f"wf_pad_edge_{t}"] = [c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_int, c_int, c_vp]
+        sig[f"wf_planes_to_raster_{t}"] = [c_vpp, c_int, c_i64, c_int, c_int, c_vp, c_vp]
     sig["wf_ipc_export"] = [c_vp, c_vp, ctypes.POINTER(c_u64)]
     sig["wf_ipc_open"] = [c_vp, ctypes.POINTER(c_vp)]
     sig["wf_ipc_close"] = [c_vp]

@@ -590,6 +590,57 @@ int wf_u8_to_f32(const uint8_t* in, int64_t in_pitch, int h, int w, float* out,
 WF_QUANTIZE(wf_quantize_f32, float)
 WF_QUANTIZE(wf_quantize_f64, double)
 
+// ---- PNM front end (raster.cu) ----------------------------------------------
+#define WF_RASTER_TO_PLANE(NAME, T)                                                           \
+  int NAME(const uint8_t* raster, int h, int w, int channels, int channel, T* out,             \
+           int64_t out_pitch, int out_h, int out_w, void* stream) {                            \
+    if (h < 1 || w < 1 || channels < 1) return fail(WF_ERR_VALUE, "empty raster");            \
+    if (channel < 0 || channel >= channels)                                                    \
+      return fail(WF_ERR_CHANNEL, "channel %d of %d", channel, channels);                     \
+    if (out_w < w || out_h < h)                                                                \
+      return fail(WF_ERR_VALUE, "cannot pad %dx%d down to %dx%d", w, h, out_w, out_h);        \
+    if (!raster || !out || out_pitch < out_w) return fail(WF_ERR_VALUE, "bad plane arguments"); \
+    cudaError_t e = wf::launch_raster_to_plane<T>(raster, h, w, channels, channel, out,        \
+                                                  out_pitch, out_h, out_w, (cudaStream_t)stream); \
+    if (e == cudaSuccess) ++g_launches;                                                        \
+    return cuda_status(e, #NAME);                                                              \
+  }
+WF_RASTER_TO_PLANE(wf_raster_to_plane_f32, float)
+WF_RASTER_TO_PLANE(wf_raster_to_plane_f64, double)
+
+#define WF_PAD_EDGE(NAME, T)                                                                   \
+  int NAME(const T* in, int64_t in_pitch, int h, int w, T* out, int64_t out_pitch, int out_h,  \
+           int out_w, void* stream) {                                                          \
+    if (h < 1 || w < 1) return fail(WF_ERR_VALUE, "empty plane");                             \
+    if (out_w < w || out_h < h)                                                                \
+      return fail(WF_ERR_VALUE, "cannot pad %dx%d down to %dx%d", w, h, out_w, out_h);        \
+    if (!in || !out || in_pitch < w || out_pitch < out_w)                                      \
+      return fail(WF_ERR_VALUE, "bad plane arguments");                                       \
+    cudaError_t e = wf::launch_pad_edge<T>(in, in_pitch, h, w, out, out_pitch, out_h, out_w,   \
+                                           (cudaStream_t)stream);                              \
+    if (e == cudaSuccess) ++g_launches;                                                        \
+    return cuda_status(e, #NAME);                                                              \
+  }
+WF_PAD_EDGE(wf_pad_edge_f32, float)
+WF_PAD_EDGE(wf_pad_edge_f64, double)
+
+#define WF_PLANES_TO_RASTER(NAME, T)                                                           \
+  int NAME(const T* const* planes, int nplanes, int64_t pitch, int h, int w, uint8_t* raster,  \
+           void* stream) {                                                                     \
+    if (nplanes < 1 || nplanes > wf::kMaxRasterPlanes)                                         \
+      return fail(WF_ERR_VALUE, "%d planes (1..%d)", nplanes, wf::kMaxRasterPlanes);          \
+    if (h < 1 || w < 1) return fail(WF_ERR_VALUE, "empty raster");                            \
+    if (!planes || !raster || pitch < w) return fail(WF_ERR_VALUE, "bad raster arguments");   \
+    for (int k = 0; k < nplanes; ++k)                                                          \
+      if (!planes[k]) return fail(WF_ERR_VALUE, "null plane pointer %d", k);                  \
+    cudaError_t e = wf::launch_planes_to_raster<T>(planes, nplanes, pitch, h, w, raster,       \
+                                                   (cudaStream_t)stream);                      \
+    if (e == cudaSuccess) ++g_launches;                                                        \
+    return cuda_status(e, #NAME);                                                              \
+  }
+WF_PLANES_TO_RASTER(wf_planes_to_raster_f32, float)
+WF_PLANES_TO_RASTER(wf_planes_to_raster_f64, double)
+
 #define WF_DWT2D(NAME, T, INV)                                                               \
   int NAME(int kind, const T* in, int64_t in_pitch, T* out, int64_t out_pitch, int h, int w, \
            void* stream) {                                                                   \

@@ -60,6 +60,19 @@ template <typename T>
 cudaError_t launch_quantize(const T* in, long long ip, int h, int w, uint8_t* out, long long op,
                             cudaStream_t s);
 
+// PNM front end (raster.cu): to_plane + pad_edge, pad_edge, quantize +
+// interleave (imageio.py:104-123, tiling.py:285-310, cli.py:135-144).
+constexpr int kMaxRasterPlanes = 8;
+template <typename To>
+cudaError_t launch_raster_to_plane(const uint8_t* r, int h, int w, int ch, int channel, To* out,
+                                   long long op, int oh, int ow, cudaStream_t s);
+template <typename T>
+cudaError_t launch_pad_edge(const T* in, long long ip, int h, int w, T* out, long long op, int oh,
+                            int ow, cudaStream_t s);
+template <typename T>
+cudaError_t launch_planes_to_raster(const T* const* planes, int np, long long pitch, int h, int w,
+                                    uint8_t* r, cudaStream_t s);
+
 // Standalone transforms (materialise coefficients; wavelet.py:131-164).
 template <typename T>
 cudaError_t launch_dwt2d(int kind, bool inverse, const T* in, long long in_pitch, T* out,

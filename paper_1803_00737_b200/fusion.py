@@ -242,7 +242,11 @@ def quantize(plane):
     """imageio.py:115-123: clamp to [0, 255], then floor(x + 0.5), as uint8 --
     in float32 for float32 planes and float64 otherwise, like numpy."""
     is_t = _is_tensor(plane)
-    out = _quantize_dev(_device.to_device(plane, _device.np_out_dtype(plane)))
+    t = _device.to_device(plane, _device.np_out_dtype(plane))
+    shape = tuple(t.shape)
+    if t.dim() != 2:  # any shape: quantize is elementwise
+        t = t.reshape(1, -1)
+    out = _quantize_dev(t).reshape(shape)
     return out if is_t else out.cpu().numpy()
 
 

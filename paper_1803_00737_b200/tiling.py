@@ -79,24 +79,73 @@ def _shape(x):
     return tuple(x.shape) if isinstance(x, torch.Tensor) else np.shape(x)
 
 
+def pad_edge(plane, out_w: int, out_h: int):
+    """tiling.py:285-293: grow a plane to out_w x out_h by replicating its last
+    row and column (np.pad mode="edge"); always a fresh array. One launch of
+    wf_pad_edge_* on the GPU; numpy in -> numpy out, tensor in -> tensor out."""
+    is_t = isinstance(plane, torch.Tensor)
+    if not is_t:
+        plane = np.asarray(plane)
+    h, w = _shape(plane)
+    if out_w < w or out_h < h:
+        raise ValueError(f"cannot pad {w}x{h} down to {out_w}x{out_h}")
+    dt = _device.np_out_dtype(plane)
+    src = _device.to_device(plane, dt)
+    if (out_w, out_h) == (w, h):
+        out = src.clone() if src is plane else src  # always a fresh array (plane.copy())
+    else:
+        out = torch.empty((out_h, out_w), dtype=src.dtype, device=src.device)
+        fn = _native.load().wf_pad_edge_f32 if dt == np.float32 else _native.load().wf_pad_edge_f64
+        _native.check(fn(src.data_ptr(), src.stride(0), h, w, out.data_ptr(), out_w, out_h, out_w,
+                         _device.stream_ptr()))
+    return out if is_t else out.cpu().numpy()
+
+
+def pad_inputs(pan, ms, grid_w: int, grid_h: int):
+    """tiling.py:296-310: edge-pad the PAN to grid-compatible dimensions and
+    every band in proportion ((bw * pw + w - 1) // w per axis), so the bands
+    keep covering the same region. Returns (pan, list(ms)) unchanged when no
+    padding is needed."""
+    h, w = _shape(pan)
+    pw, ph = padded_dims(w, h, grid_w, grid_h)
+    if (pw, ph) == (w, h):
+        return pan, list(ms)
+    bands = []
+    for band in ms:
+        bh, bw = _shape(band)
+        bands.append(pad_edge(band, (bw * pw + w - 1) // w, (bh * ph + h - 1) // h))
+    return pad_edge(pan, pw, ph), bands
+
+
 def _window_fuse(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
-                 out: list[torch.Tensor], grid: TileGrid) -> None:
+                 out: list[torch.Tensor], grid: TileGrid, exact: bool = False) -> None:
     """One fused launch per tile on strided windows of the device scene; each
-    tile wraps periodically within itself."""
+    tile wraps periodically within itself. exact=True runs the reference's
+    float64 operation order per tile and band (wf_fuse_dwt_exact_*)."""
     lib = _native.load()
     esz = pan.element_size()
-    fn = {torch.float32: lib.wf_fuse_bands_f32, torch.float64: lib.wf_fuse_bands_f64,
-          torch.uint8: lib.wf_fuse_bands_u8}[pan.dtype]
     tw, th = grid.pan_tile_w, grid.pan_tile_h
     pp, mp, op = pan.stride(0), ms[0].stride(0), out[0].stride(0)
     s = _device.stream_ptr()
+    code = KIND_CODE[kind]
+    if exact:
+        fn = lib.wf_fuse_dwt_exact_f32 if pan.dtype == torch.float32 else lib.wf_fuse_dwt_exact_f64
+        ws = torch.empty((th, tw), dtype=torch.float64, device=pan.device)
+    else:
+        fn = {torch.float32: lib.wf_fuse_bands_f32, torch.float64: lib.wf_fuse_bands_f64,
+              torch.uint8: lib.wf_fuse_bands_u8}[pan.dtype]
     for row in range(grid.grid_h):
         for col in range(grid.grid_w):
             r0, c0 = row * th, col * tw
             pan_p = pan.data_ptr() + (r0 * pp + c0) * esz
-            ms_p = _native.ptr_array([m.data_ptr() + ((r0 // 2) * mp + c0 // 2) * esz for m in ms])
-            out_p = _native.ptr_array([o.data_ptr() + (r0 * op + c0) * esz for o in out])
-            _native.check(fn(KIND_CODE[kind], pan_p, pp, ms_p, mp, out_p, op, len(ms), th, tw, s))
+            ms_a = [m.data_ptr() + ((r0 // 2) * mp + c0 // 2) * esz for m in ms]
+            out_a = [o.data_ptr() + (r0 * op + c0) * esz for o in out]
+            if exact:
+                for m_p, o_p in zip(ms_a, out_a):
+                    _native.check(fn(code, pan_p, pp, m_p, mp, o_p, op, th, tw, ws.data_ptr(), s))
+            else:
+                _native.check(fn(code, pan_p, pp, _native.ptr_array(ms_a), mp,
+                                 _native.ptr_array(out_a), op, len(ms), th, tw, s))
 
 
 def _u8_windows_ok(grid: TileGrid, kind: WaveletKind) -> bool:
@@ -106,13 +155,15 @@ def _u8_windows_ok(grid: TileGrid, kind: WaveletKind) -> bool:
 
 
 def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
-               transfer_8bpp: bool = False):
+               transfer_8bpp: bool = False, *, exact: bool = False):
     """tiling.py:213-273 for DwtReplace. `workers` is accepted for signature
     compatibility (the GPU fuses tiles, not a thread pool). Plain mode
     resamples bands globally, then fuses every tile with per-tile wrap (float
-    output, pan dtype). transfer_8bpp reproduces the distributed pipeline:
-    inputs quantised to uint8 (wire_planes, tiling.py:192-210), each tile
-    fused in float32 and quantised (tiling.py:163-172, 268-269)."""
+    output, pan dtype); exact=True fuses each tile in the reference's own
+    float64 operation order (bit-identical to the reference). transfer_8bpp
+    reproduces the distributed pipeline: inputs quantised to uint8
+    (wire_planes, tiling.py:192-210), each tile fused in float32 and quantised
+    (tiling.py:163-172, 268-269)."""
     if workers < 1:
         raise ValueError(f"workers {workers} must be >= 1")
     is_t = isinstance(pan, torch.Tensor)
@@ -161,6 +212,6 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
     pan_t = _device.to_device(pan, dt)
     ms_t = [_device.to_device(b, dt) for b in sized]
     outs = [torch.empty_like(pan_t) for _ in ms_t]
-    _window_fuse(kind, pan_t, ms_t, outs, grid)
+    _window_fuse(kind, pan_t, ms_t, outs, grid, exact=exact)
     return outs if is_t else [o.cpu().numpy() for o in outs]
 

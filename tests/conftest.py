@@ -51,3 +51,8 @@ def golden_transforms():
 @pytest.fixture(scope="session")
 def golden_metrics():
     return Golden("metrics")
+
+
+@pytest.fixture(scope="session")
+def golden_pnm():
+    return Golden("pnm")

@@ -206,11 +206,75 @@ def tiled_golden():
     np.savez_compressed(OUT / "tiled.npz", **data)
 
 
+def _pgm(a: np.ndarray, comment: bytes = b"") -> bytes:
+    h, w = a.shape[:2]
+    magic = b"P5" if a.ndim == 2 else b"P6"
+    return magic + b"\n" + comment + b"%d %d\n255\n" % (w, h) + np.ascontiguousarray(a).tobytes()
+
+
+def pnm_golden():
+    """The reference CLI end to end (cli.main(["fuse", ...]) on temp files):
+    PNM inputs -> edge padding -> fuse_tiled -> crop -> quantize -> PNM
+    outputs, recorded byte for byte. Also pad_edge / pad_inputs outputs."""
+    import tempfile
+
+    from wavefuse import cli, tiling
+
+    rng = np.random.default_rng(5)
+    data = {}
+    # (name, pan h, pan w, band shapes, one PPM?, grid)
+    cases = [("rgb", 50, 70, (25, 35), True, "2x2"),        # padded to 52x72
+             ("gray2", 48, 64, (24, 32), False, "1x1"),      # 2 PGM bands -> 2 PGMs
+             ("gray1", 40, 66, (20, 33), False, "2x1"),      # 1 band -> 1 PGM
+             ("rs", 44, 60, (13, 17), True, "2x2")]          # bands resampled
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, h, w, bshape, ppm, grid in cases:
+            pan = rng.integers(0, 256, (h, w), dtype=np.uint8)
+            pan_b = _pgm(pan, b"# pan with a comment\n")
+            nb = 3 if ppm else (2 if name == "gray2" else 1)
+            bands = [rng.integers(0, 256, bshape, dtype=np.uint8) for _ in range(nb)]
+            ms_b = [_pgm(np.stack(bands, axis=-1))] if ppm else [_pgm(b) for b in bands]
+            data[f"{name}/pan"] = np.frombuffer(pan_b, np.uint8)
+            data[f"{name}/grid"] = np.array([int(v) for v in grid.split("x")])
+            for k, m in enumerate(ms_b):
+                data[f"{name}/ms{k}"] = np.frombuffer(m, np.uint8)
+            (Path(tmp) / "pan.pgm").write_bytes(pan_b)
+            ms_paths = []
+            for k, m in enumerate(ms_b):
+                path = Path(tmp) / f"ms{k}.{'ppm' if ppm else 'pgm'}"
+                path.write_bytes(m)
+                ms_paths.append(str(path))
+            for method in ("hdwt", "ddwt"):
+                out = Path(tmp) / f"{name}_{method}.{'ppm' if ppm else 'pgm'}"
+                argv = ["fuse", "--pan", str(Path(tmp) / "pan.pgm"), "--method", method,
+                        "--grid", grid, "--workers", "2", "--out", str(out)]
+                for mp in ms_paths:
+                    argv += ["--ms", mp]
+                assert cli.main(argv) == 0
+                outs = [out] if nb in (1, 3) else [
+                    out.with_name(f"{out.stem}_b{k}.pgm") for k in range(nb)]
+                for k, o in enumerate(outs):
+                    data[f"{name}/{method}/out{k}"] = np.frombuffer(o.read_bytes(), np.uint8)
+    for name, (h, w), (ow, oh) in [("p0", (5, 7), (9, 8)), ("p1", (6, 4), (4, 6)),
+                                   ("p2", (1, 3), (4, 2))]:
+        plane = rng.uniform(0, 255, (h, w)).astype(np.float32)
+        data[f"pad/{name}/in"] = plane
+        data[f"pad/{name}/out"] = tiling.pad_edge(plane, ow, oh)
+    pan = rng.uniform(0, 255, (50, 70)).astype(np.float32)
+    ms = [rng.uniform(0, 255, (25, 35)).astype(np.float32), rng.uniform(0, 255, (13, 17))
+          .astype(np.float32)]
+    pp, mp_ = tiling.pad_inputs(pan, ms, 4, 3)
+    data["padin/pan"], data["padin/ms0"], data["padin/ms1"] = pan, ms[0], ms[1]
+    data["padin/out_pan"], data["padin/out_ms0"], data["padin/out_ms1"] = pp, mp_[0], mp_[1]
+    np.savez_compressed(OUT / "pnm.npz", **data)
+
+
 if __name__ == "__main__":
     fusion_golden()
     transform_golden()
     metrics_golden()
     quantized_golden()
     tiled_golden()
+    pnm_golden()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

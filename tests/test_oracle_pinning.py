@@ -247,3 +247,37 @@ def test_quantized_path_matches_reference_golden():
             got = O.fuse_quantized(pan, ms, kind)
             for b, o in enumerate(got):
                 assert np.array_equal(o, g[f"t{k}/{kind}/out{b}"]), (k, kind, b)
+
+
+# --- PNM front end (oracle/cpu_raster.py) against the reference CLI's files ---
+
+from oracle import cpu_raster as R  # noqa: E402
+
+PNM_CASES = ("rgb", "gray2", "gray1", "rs")
+
+
+def _pnm_inputs(g, name):
+    ms = [g[k].tobytes() for k in sorted(k for k in g.keys() if k.startswith(f"{name}/ms"))]
+    return g[f"{name}/pan"].tobytes(), ms, [int(v) for v in g[f"{name}/grid"]]
+
+
+@pytest.mark.parametrize("name", PNM_CASES)
+@pytest.mark.parametrize("method,kind", [("hdwt", "haar"), ("ddwt", "daub4")])
+def test_cli_fuse_oracle_matches_reference_files(golden_pnm, name, method, kind):
+    pan, ms, (gw, gh) = _pnm_inputs(golden_pnm, name)
+    got = R.cli_fuse(pan, ms, kind, gw, gh)
+    want = [golden_pnm[k].tobytes() for k in sorted(
+        k for k in golden_pnm.keys() if k.startswith(f"{name}/{method}/out"))]
+    assert got == want
+
+
+def test_pad_oracle_matches_reference(golden_pnm):
+    for name in ("p0", "p1", "p2"):
+        src, want = golden_pnm[f"pad/{name}/in"], golden_pnm[f"pad/{name}/out"]
+        got = R.pad_edge(src, want.shape[1], want.shape[0])
+        assert got.dtype == want.dtype and np.array_equal(got, want)
+    pan, ms = golden_pnm["padin/pan"], [golden_pnm["padin/ms0"], golden_pnm["padin/ms1"]]
+    pp, mp = R.pad_inputs(pan, ms, 4, 3)
+    assert np.array_equal(pp, golden_pnm["padin/out_pan"])
+    assert np.array_equal(mp[0], golden_pnm["padin/out_ms0"])
+    assert np.array_equal(mp[1], golden_pnm["padin/out_ms1"])
