@@ -99,12 +99,25 @@ def _install():
 
     Bn.fuse_tiled = cpu_tiled
 
+    # the PNM front end (imageio.py) and the CLI's data
+    # path (cli.py:113-165 binds these names at import)
+    import wavefuse.cli as Cli
+    import wavefuse.imageio as Io
+
+    for name in ("read_pnm", "write_pnm", "to_plane", "quantize"):
+        setattr(Io, name, translate(getattr(wf, name), name))
+        setattr(Cli, name, getattr(Io, name))
+    T.pad_edge = translate(wf.pad_edge, "pad_edge")
+    T.pad_inputs = translate(wf.pad_inputs, "pad_inputs")
+    Cli.pad_inputs = T.pad_inputs
+    Cli.fuse_tiled = fuse_tiled
+
     for name in ("fuse_dwt", "resample_bilinear", "dwt1d_forward", "dwt1d_inverse",
                  "dwt2d_forward", "dwt2d_inverse", "degrade", "q_index", "ergas", "d_lambda",
-                 "d_s", "qnr"):
+                 "d_s", "qnr", "read_pnm", "write_pnm", "to_plane", "quantize", "pad_inputs"):
         if hasattr(wavefuse, name):
             setattr(wavefuse, name, getattr(F, name, None) or getattr(Wv, name, None)
-                    or getattr(M, name))
+                    or getattr(Io, name, None) or getattr(T, name, None) or getattr(M, name))
 
 
 def pytest_configure(config):
