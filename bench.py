@@ -249,19 +249,25 @@ def measure_device(scene, kind, steps, warmup, dist, world, dev_index):
     return ms, launches, clk.summary()
 
 
-def measure_e2e(scene, kind, steps, dist):
-    """End to end through the public host-buffer C ABI (wf_fuse_host_f32):
-    every step copies the scene's inputs from pinned host memory, fuses, and
-    reads every fused band back into pinned host memory."""
+def measure_e2e(scene, kind, steps, dist, pan_d=None, ms_d=None, ref_out=None):
+    """End to end through the public host-buffer C ABI (wf_fuse_host_f32, or
+    wf_fuse_host_u8 for uint8 planes): every step copies the scene's inputs
+    from pinned host memory, fuses, and reads every fused band back into
+    pinned host memory."""
     import torch
 
     from paper_1803_00737_b200 import _native
     from paper_1803_00737_b200.wavelet import KIND_CODE
 
     lib = _native.load()
-    pan_h = scene.pan.cpu().pin_memory()
-    ms_h = [m.cpu().pin_memory() for m in scene.ms]
-    out_h = [torch.empty(scene.pan.shape, dtype=torch.float32).pin_memory() for _ in scene.ms]
+    pan_d = scene.pan if pan_d is None else pan_d
+    ms_d = scene.ms if ms_d is None else ms_d
+    ref_out = scene.out if ref_out is None else ref_out
+    esz = pan_d.element_size()
+    host_fn = lib.wf_fuse_host_u8 if pan_d.dtype == torch.uint8 else lib.wf_fuse_host_f32
+    pan_h = pan_d.cpu().pin_memory()
+    ms_h = [m.cpu().pin_memory() for m in ms_d]
+    out_h = [torch.empty(pan_d.shape, dtype=pan_d.dtype).pin_memory() for _ in ms_d]
     ctx = lib.wf_ctx_create(torch.cuda.current_device(), 1024)
     ms_p = _native.ptr_array([m.data_ptr() for m in ms_h])
     out_p = _native.ptr_array([o.data_ptr() for o in out_h])
@@ -269,8 +275,7 @@ def measure_e2e(scene, kind, steps, dist):
     code = KIND_CODE[kind]
 
     def step():
-        _native.check(lib.wf_fuse_host_f32(ctx, code, pan_h.data_ptr(), ms_p, out_p, len(ms_h),
-                                           h, w))
+        _native.check(host_fn(ctx, code, pan_h.data_ptr(), ms_p, out_p, len(ms_h), h, w))
 
     step()
     torch.cuda.synchronize()
@@ -286,11 +291,11 @@ def measure_e2e(scene, kind, steps, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
     # spot-check the e2e result against the device-resident one
-    ok = bool(torch.equal(out_h[0][:64].cuda(), scene.out[0][:64]))
+    ok = bool(torch.equal(out_h[0][:64].cuda(), ref_out[0][:64]))
     lib.wf_ctx_destroy(ctx)
-    halo = 4 * w * 4 if kind.value == "daub4" else 0
-    h2d = pan_h.numel() * 4 + sum(m.numel() * 4 for m in ms_h) + halo * (h // 1024 + 1)
-    d2h = sum(o.numel() * 4 for o in out_h)
+    halo = 4 * w * esz if kind.value == "daub4" else 0
+    h2d = pan_h.numel() * esz + sum(m.numel() * esz for m in ms_h) + halo * (h // 1024 + 1)
+    d2h = sum(o.numel() * esz for o in out_h)
     return sec, h2d, d2h, ok
 
 
@@ -391,12 +396,21 @@ def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
             ms_t = float(t.item())
         per = ms_t / steps
         achieved = nbytes / (per * 1e-3) / 1e9
+        e2e_steps = max(2, min(steps, 5))
+        sec, h2d, d2h, ok = measure_e2e(scene, kind, e2e_steps, dist, pan, ms, [o.clone() for o in out])
         res[kind.value] = {
             "value": round(world * h * w / (per * 1e-3) / 1e6, 3),
             "ms_per_step": round(per, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "algorithmic_bytes_per_launch": nbytes},
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "kernel": ("fuse_haar_u8_kernel<B=6> (16-bit lanes)"
+                                    if kind is WaveletKind.HAAR
+                                    else "fuse_d4_tma_kernel<u8,B=6,4 consumer warps>")},
+            "e2e": {"value": round(world * h * w * e2e_steps / sec / 1e6, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "wf_fuse_host_u8 (C ABI, pinned host buffers, strips of 1024 rows)",
+                    "matches_device_result": ok},
         }
     return {"unit": UNIT, "dtype": "u8 in/out, f32 arithmetic", **res}
 
@@ -440,7 +454,8 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": ncu_traffic(f"fuse_{kind.value}_b6"),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "algorithmic_bytes_per_launch": nbytes,
-                "kernel": f"fuse_{'haar' if kind is WaveletKind.HAAR else 'd4'}_kernel<f32,B=6>",
+                "kernel": ("fuse_haar_kernel<f32,B=6>" if kind is WaveletKind.HAAR
+                           else "fuse_d4_tma_kernel<f32,B=6,4 consumer warps>"),
             },
             "e2e": {
                 "value": round(world * H * W * e2e_steps / sec / 1e6, 3),
