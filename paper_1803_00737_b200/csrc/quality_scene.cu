@@ -30,7 +30,10 @@
 // cross-lane / cross-block combination is float64; on 0..255 data the report
 // agrees with the float64 reference to ~1e-8 (tests check 1e-6, the north
 // star asks for 4 decimals).
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "wf_common.cuh"
 #include "wf_kernels.h"
@@ -44,9 +47,12 @@ constexpr int kQsWarps = 7;
 constexpr int kQsCols = 32 * kQsWarps;   // 224 PAN columns per CTA
 constexpr int kQsMsw = kQsCols / 2 + 8;  // staged MS segment (4-col halo each side)
 
+#ifndef WF_QS_STAGES
+#define WF_QS_STAGES 4
+#endif
 template <int NB>
 struct QsCfg {
-  static constexpr int S = NB <= 6 ? 4 : 3;                      // ring depth (row pairs)
+  static constexpr int S = NB <= 6 ? WF_QS_STAGES : 3;           // ring depth (row pairs)
   static constexpr int MSOFF = 2 * (NB + 1) * kQsCols;           // floats before the MS rows
   static constexpr int SLOT = MSOFF + 3 * NB * kQsMsw;           // floats per slot
 };
@@ -105,6 +111,18 @@ __device__ __forceinline__ void two_sum(float a, float b, float& s, float& t) {
   s = a + b;
   const float bb = s - a;
   t = (a - (s - bb)) + (b - bb);
+}
+
+// The degraded-PAN shift of a low-res block as the exact float pair (hi, lo)
+// of its 2x2 sum (p00 + p10, p01 + p11 by TwoSum, then across), formed by the
+// same TwoSum sequence the main loops use, so a constant region gives exactly
+// zero deltas.
+__device__ __forceinline__ void shift_pan(float4 p, float& kph, float& kpl) {
+  float s, t, s2, t2, T;
+  two_sum(p.x, p.y, s, t);
+  two_sum(p.z, p.w, s2, t2);
+  two_sum(s, s2, kph, T);
+  kpl = T + (t + t2);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -225,10 +243,13 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
   // The degraded-PAN shift is kept as the exact float pair (hi, lo) of its
   // 2x2 sum, formed by the same TwoSum sequence the main loop uses, so a
   // constant region gives exactly zero deltas.
-  auto load_shifts = [&](int tile, float (&kmv)[NB], float& kph, float& kpl) {
+  // Only raw loads here; the values are consumed a whole half-tile later
+  // (shift_pan at the next tile's start), so the global-load latency never
+  // stalls a warp that still holds a ring slot.
+  auto load_shifts = [&](int tile, float (&kmv)[NB], float4& praw) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) kmv[k] = 0.f;
-    kph = kpl = 0.f;
+    praw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (tile >= ntiles) return;
     const int br = tile / a.ncx, cx = tile % a.ncx;
     const int bc = cx * kQsWarps + warp;
@@ -238,16 +259,13 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
 #pragma unroll
     for (int k = 0; k < NB; ++k)
       kmv[k] = __ldg(a.M[k] + min(my, (long long)a.Hh - 1) * a.mp + min(mx, (long long)a.Wh - 1));
-    if (py + 1 < a.H && px + 1 < a.W) {
-      float s, t, s2, t2, T;
-      two_sum(__ldg(a.P + py * a.pp + px), __ldg(a.P + (py + 1) * a.pp + px), s, t);
-      two_sum(__ldg(a.P + py * a.pp + px + 1), __ldg(a.P + (py + 1) * a.pp + px + 1), s2, t2);
-      two_sum(s, s2, kph, T);
-      kpl = T + (t + t2);
-    }
+    if (py + 1 < a.H && px + 1 < a.W)
+      praw = make_float4(__ldg(a.P + py * a.pp + px), __ldg(a.P + (py + 1) * a.pp + px),
+                         __ldg(a.P + py * a.pp + px + 1), __ldg(a.P + (py + 1) * a.pp + px + 1));
   };
-  float km_next[NB], kph_next, kpl_next;
-  load_shifts(blockIdx.x, km_next, kph_next, kpl_next);
+  float km_next[NB];
+  float4 praw_next;
+  load_shifts(blockIdx.x, km_next, praw_next);
 
   int g = 0;
   int parity = 0;
@@ -270,8 +288,8 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
     const int lr = br >> 1, lc = bc >> 1;
     const bool low_ok = blk_ok && lr < a.nbr_l && lc < a.nbc_l;
 
-    float km[NB];
-    const float kph = kph_next, kpl = kpl_next;
+    float km[NB], kph, kpl;
+    shift_pan(praw_next, kph, kpl);
 #pragma unroll
     for (int k = 0; k < NB; ++k) km[k] = km_next[k];
 
@@ -301,7 +319,7 @@ __global__ void __launch_bounds__(32 * (kQsWarps + 1), 1)
 
     for (int t = 0; t < 16; ++t, ++g) {
       const int s = g % S;
-      if (t == 8) load_shifts(tile + gridDim.x, km_next, kph_next, kpl_next);
+      if (t == 8) load_shifts(tile + gridDim.x, km_next, praw_next);
       tma::mbar_wait(&full[s], (g / S) & 1);
       const float* slot = ring + (size_t)s * C::SLOT;
       const float* msr = slot + C::MSOFF;
@@ -620,6 +638,636 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Role-split variant (the default): three consumer warps per 32x32 block
+// column instead of one, so each thread carries a third of the per-lane state
+// (<= 128 registers) and 16 warps per SM hide the latency that left the
+// one-warp-per-block kernel above issue-starved at 8 warps per SM:
+//   role F: S1/S2 of the fused planes and the PAN -- sum dF_k, sum dF_k dF_l,
+//           sum dF_k dP, sum dP, sum dP^2 (FFMA2 over band pairs);
+//   role U: the bilinear upsample U_k and sum dU_k, sum dU_k dU_l,
+//           sum dF_k dU_k;
+//   role L: the 2x2 cells (low-res D_s moments and the ERGAS sums). Even
+//           lanes finish the first half of the bands and odd lanes the
+//           second half (after one exchange of the per-column TwoSums), so
+//           no lane idles through the cell arithmetic.
+// The three warps of a block column meet at a named barrier; role F then
+// scores the block's Q pairs from the shared float64 sums. Results are the
+// same quantities in the same float32/float64 arithmetic as above.
+// ---------------------------------------------------------------------------
+constexpr int kQ2Bc = 5;                 // block columns per CTA
+constexpr int kQ2Cols = 32 * kQ2Bc;      // 160 PAN columns per tile
+constexpr int kQ2Msw = 96;               // staged MS segment: 80 cols + halo, one 384-B box
+constexpr int kQ2Cons = 3 * kQ2Bc;       // consumer warps
+constexpr int kQ2Prod = 1;               // producer warps
+constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
+constexpr int kQ2TrRows = 16;            // transpose chunk (rows of 32 lanes)
+
+#ifndef WF_Q2_STAGES
+#define WF_Q2_STAGES 2
+#endif
+// Tensor maps of the scene planes (2-D, float32): the producer moves a
+// 2-row x 160-column box of each PAN-resolution plane and one 96-column MS
+// row per band with one UTMALDG each.
+struct Q2Maps {
+  CUtensorMap f[kMaxBandsPerLaunch];
+  CUtensorMap p;
+  CUtensorMap m[kMaxBandsPerLaunch];
+};
+
+template <int NB>
+struct Q2Cfg {
+  static constexpr int S = WF_Q2_STAGES;
+  // A stage is PAIRS row pairs (8 PAN rows): plane q (F_0..F_{NB-1}, P) as a
+  // dense [8][kQ2Cols] box at q * PLANE, then per band the MSR = 6 MS rows
+  // i0 + 4u - 1 .. i0 + 4u + 4 the stage's bilinear and 2x2 cells touch
+  // ([NB][6][kQ2Msw]; rows outside the image arrive zero-filled and are
+  // never read: the consumers clamp the row index first). One tensor copy
+  // per plane and per band: 13 copies per 8 rows at B = 6.
+  static constexpr int PAIRS = 4;
+  static constexpr int MSR = PAIRS + 2;
+  static constexpr int PLANE = 2 * PAIRS * kQ2Cols;
+  static constexpr int MSOFF = (NB + 1) * PLANE;
+  static constexpr int SLOT = MSOFF + NB * MSR * kQ2Msw;
+  static constexpr int NBE = NB + (NB & 1);  // bands padded to even (role L halves)
+  static constexpr int H = NBE / 2;
+  static constexpr int NBP = NBE / 2;        // float2 band pairs
+  static constexpr int DS = QsLayout<NB>::NV + QsLayout<NB>::NP + NB;  // doubles per block
+  // upper-triangle products as float2 pairs: row k starts at l = k (k even)
+  // or k + 1 (k odd, with the diagonal kept as a scalar)
+  __host__ __device__ static constexpr int start(int k) { return (k & 1) ? k + 1 : k; }
+  __host__ __device__ static constexpr int npairs(int k) { return (NBE - start(k)) / 2; }
+  __host__ __device__ static constexpr int base(int k) {
+    int b = 0;
+    for (int i = 0; i < k; ++i) b += npairs(i);
+    return b;
+  }
+  static constexpr int NT2 = base(NB);  // pair accumulators of the triangle
+  static constexpr int ND = NB / 2;     // odd-k diagonals
+};
+
+// lane-sum `n` (<= 32) rows of per-lane floats into ds[0..n) (float64)
+__device__ __forceinline__ void q2_flush(float* tr, int n, double* ds, int lane) {
+  __syncwarp();
+  for (int v = lane; v < n; v += 32) ds[v] = (double)lane_sum32(tr + v * kTrPad);
+  __syncwarp();
+}
+
+// Transpose-and-sum NR per-lane values v[0..NR) into ds[idx(r)] (float64),
+// in chunks of kQ2TrRows rows through the warp's buffer.
+template <int NR, typename Idx>
+__device__ __forceinline__ void q2_reduce(float* tr, double* ds, int lane, const float (&v)[NR],
+                                          Idx idx) {
+#pragma unroll
+  for (int c0 = 0; c0 < NR; c0 += kQ2TrRows) {
+    constexpr int kRows = kQ2TrRows;
+    const int n = NR - c0 < kRows ? NR - c0 : kRows;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+      if (c0 + r < NR) tr[r * kTrPad + lane] = v[c0 + r];
+    __syncwarp();
+    for (int w = lane; w < n; w += 32) ds[idx(c0 + w)] = (double)lane_sum32(tr + w * kTrPad);
+    __syncwarp();
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kQ2Threads, 1)
+    quality_split_kernel(const QsArgs a, const __grid_constant__ Q2Maps maps, double* part_q,
+                         double* part_low, double* part_erg, int* undecidable) {
+  using L = QsLayout<NB>;
+  using C = Q2Cfg<NB>;
+  constexpr int S = C::S, NBE = C::NBE, H = C::H, NBP = C::NBP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* ring = reinterpret_cast<float*>(  // tensor-copy destinations: 128-byte aligned
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * C::SLOT);
+  uint64_t* empty = full + S;
+  double* qw = reinterpret_cast<double*>(empty + S);  // [2][kQ2Bc][NQ]
+  double* ew = qw + 2 * kQ2Bc * L::NQ;                 // [2][kQ2Bc][NERG]
+  double* dsb = ew + 2 * kQ2Bc * L::NERG;              // [2][kQ2Bc][DS]
+  float* trs = reinterpret_cast<float*>(                // [kQ2Cons][kQ2TrRows][kTrPad]
+      (reinterpret_cast<uintptr_t>(dsb + 2 * kQ2Bc * C::DS) + 15) & ~uintptr_t(15));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = a.nbr * a.ncx;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tma::mbar_init(&full[s], kQ2Prod);
+      tma::mbar_init(&empty[s], kQ2Cons);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kQ2Cons) {
+    // ---------------------------- producer --------------------------------
+    constexpr uint32_t kStageBytes = (uint32_t)C::SLOT * 4u;
+    int g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int br = tile / a.ncx, cx = tile % a.ncx;
+      const int col0 = cx * kQ2Cols;
+      const int i0 = 16 * br;
+      const int ms0 = max((col0 >> 1) - 4, 0);
+      for (int u = 0; u < 16 / C::PAIRS; ++u, ++g) {
+        const int s = g % S, r = g / S;
+        if (r > 0 && lane == 0) tma::mbar_wait(&empty[s], (r - 1) & 1);
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive_expect_tx(&full[s], kStageBytes);
+        __syncwarp();
+        float* slot = ring + (size_t)s * C::SLOT;
+        if (lane <= NB) {
+          const CUtensorMap* tm = &maps.p;
+#pragma unroll
+          for (int k = 0; k < NB; ++k)
+            if (lane == k) tm = &maps.f[k];
+          tma::tensor_g2s_2d(slot + lane * C::PLANE, tm, col0, 32 * br + 2 * C::PAIRS * u,
+                             &full[s]);
+        } else if (lane < 2 * NB + 1) {
+          const int k = lane - (NB + 1);
+          const CUtensorMap* tm = &maps.m[0];
+#pragma unroll
+          for (int kk = 1; kk < NB; ++kk)
+            if (k == kk) tm = &maps.m[kk];
+          tma::tensor_g2s_2d(slot + C::MSOFF + k * C::MSR * kQ2Msw, tm, ms0,
+                             i0 + C::PAIRS * u - 1, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------- consumers ----------------------------------
+  const int role = warp / kQ2Bc, bcl = warp % kQ2Bc;
+  const bool odd = (lane & 1) != 0;
+  float* tr = trs + (size_t)warp * kQ2TrRows * kTrPad;
+  // role L: local band m <-> band (m + H * odd) mod NBE; bands >= NB are
+  // padding (they read the PAN row; their sums are never reported)
+  auto band_of = [&](int m) { return (m + (odd ? H : 0)) % NBE; };
+
+  // low-res shifts (role L), one tile ahead, as in the kernel above
+  // Only raw loads here; the values are consumed a whole half-tile later
+  // (shift_pan at the next tile's start), so the global-load latency never
+  // stalls a warp that still holds a ring slot.
+  auto load_shifts = [&](int tile, float (&kmv)[NB], float4& praw) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) kmv[k] = 0.f;
+    praw = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tile >= ntiles) return;
+    const int br = tile / a.ncx, cx = tile % a.ncx;
+    const int bc = cx * kQ2Bc + bcl;
+    if (bc >= a.nbc) return;
+    const long long my = 32LL * (br >> 1), mx = 32LL * (bc >> 1);
+    const long long py = 2 * my, px = 2 * mx;
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      kmv[k] = __ldg(a.M[k] + min(my, (long long)a.Hh - 1) * a.mp + min(mx, (long long)a.Wh - 1));
+    if (py + 1 < a.H && px + 1 < a.W)
+      praw = make_float4(__ldg(a.P + py * a.pp + px), __ldg(a.P + (py + 1) * a.pp + px),
+                         __ldg(a.P + py * a.pp + px + 1), __ldg(a.P + (py + 1) * a.pp + px + 1));
+  };
+  float km_next[NB];
+  float4 praw_next = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (role == 2) load_shifts(blockIdx.x, km_next, praw_next);
+
+  int g = 0, parity = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
+    const int br = tile / a.ncx, cx = tile % a.ncx;
+    const int col0 = cx * kQ2Cols;
+    const int ncols = min(kQ2Cols, 32 * a.nbc - col0);
+    const int ms0 = max((col0 >> 1) - 4, 0);
+    const int i0 = 16 * br;  // first MS row of the tile
+    const int bc = cx * kQ2Bc + bcl;
+    const bool blk_ok = 32 * bcl < ncols;
+    const int x = 32 * bc + lane;
+    const int xl = 32 * bcl + lane;
+    const int j = x >> 1;
+    const int hx0 = (x & 1) ? min(j, a.Wh - 1) : min(max(j - 1, 0), a.Wh - 1);
+    const int hx1 = (x & 1) ? min(j + 1, a.Wh - 1) : min(j, a.Wh - 1);
+    const int rx0 = min(max(hx0 - ms0, 0), kQ2Msw - 1), rx1 = min(max(hx1 - ms0, 0), kQ2Msw - 1);
+    const int rxr = min(max(min(j, a.Wh - 1) - ms0, 0), kQ2Msw - 1);  // M(i, x/2)
+    const float hfx = (x & 1) ? 0.25f : 0.75f;
+    const int lr = br >> 1, lc = bc >> 1;
+    const bool low_ok = blk_ok && lr < a.nbr_l && lc < a.nbc_l;
+    double* ds = dsb + ((size_t)parity * kQ2Bc + bcl) * C::DS;
+
+    if (role == 0) {
+      // ------------------------------ role F ------------------------------
+      float2 a1[NBP], fp2[NBP], ff[C::NT2 > 0 ? C::NT2 : 1];
+      float fd[C::ND > 0 ? C::ND : 1];
+      float2 nkf[NBP];  // -shift, so d = f + (-k) is one FADD2
+      float a1p = 0.f, app = 0.f, kp = 0.f;
+#pragma unroll
+      for (int m = 0; m < NBP; ++m) a1[m] = fp2[m] = nkf[m] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < C::NT2; ++i) ff[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < C::ND; ++i) fd[i] = 0.f;
+      for (int u = 0; u < 16 / C::PAIRS; ++u) {
+        const int s = g % S;
+        tma::mbar_wait(&full[s], (g / S) & 1);
+        const float* slot = ring + (size_t)s * C::SLOT;
+#pragma unroll
+        for (int h = 0; h < C::PAIRS; ++h) {  // row pair h of the stage
+        const int t = C::PAIRS * u + h;
+        float fv[2][NBE], pv[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+#pragma unroll
+          for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
+          pv[p] = row[NB * C::PLANE];
+        }
+        if (h == C::PAIRS - 1) {
+          __syncwarp();
+          if (lane == 0) tma::mbar_arrive(&empty[s]);
+          ++g;
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          if (t == 0 && p == 0) {
+#pragma unroll
+            for (int m = 0; m < NBP; ++m)
+              nkf[m] = make_float2(-__shfl_sync(0xffffffffu, fv[0][2 * m], 0),
+                                   -__shfl_sync(0xffffffffu, fv[0][2 * m + 1], 0));
+            kp = __shfl_sync(0xffffffffu, pv[0], 0);
+          }
+          float2 d[NBP];
+#pragma unroll
+          for (int m = 0; m < NBP; ++m) {
+            d[m] = __fadd2_rn(make_float2(fv[p][2 * m], fv[p][2 * m + 1]), nkf[m]);
+            a1[m] = __fadd2_rn(a1[m], d[m]);
+          }
+          const float dp = pv[p] - kp;
+          a1p += dp;
+          app = fmaf(dp, dp, app);
+#pragma unroll
+          for (int m = 0; m < NBP; ++m) fp2[m] = __ffma2_rn(make_float2(dp, dp), d[m], fp2[m]);
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            const float dk = (k & 1) ? d[k >> 1].y : d[k >> 1].x;
+            if (k & 1) fd[k >> 1] = fmaf(dk, dk, fd[k >> 1]);
+#pragma unroll
+            for (int q = 0; q < C::npairs(k); ++q)
+              ff[C::base(k) + q] =
+                  __ffma2_rn(make_float2(dk, dk), d[(C::start(k) >> 1) + q], ff[C::base(k) + q]);
+          }
+        }
+        }
+      }
+      // this role's entries of S1 [F_k | U_k | P] and S2 [FF tri | UU tri |
+      // FU | FP | PP], listed as [F_k, P, FF tri, FP_k, PP]
+      constexpr int NR = NB + 1 + L::NFF + NB + 1;
+      float v[NR];
+      {
+        int r = 0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? a1[k >> 1].y : a1[k >> 1].x;
+        v[r++] = a1p;
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) {
+            const int o = l - C::start(k);
+            v[r++] = ((k & 1) && l == k) ? fd[k >> 1]
+                                         : ((o & 1) ? ff[C::base(k) + (o >> 1)].y
+                                                    : ff[C::base(k) + (o >> 1)].x);
+          }
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fp2[k >> 1].y : fp2[k >> 1].x;
+        v[r++] = app;
+      }
+      q2_reduce<NR>(tr, ds, lane, v, [&](int r) -> int {
+        if (r < NB) return r;                              // S1 F_k
+        if (r == NB) return 2 * NB;                        // S1 P
+        r -= NB + 1;
+        if (r < L::NFF) return L::NP + r;                  // S2 FF tri
+        r -= L::NFF;
+        if (r < NB) return L::NP + 2 * L::NFF + NB + r;    // S2 FP
+        return L::NP + 2 * L::NFF + 2 * NB;                // S2 PP
+      });
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) ds[L::NV + k] = -((k & 1) ? nkf[k >> 1].y : nkf[k >> 1].x);
+        ds[L::NV + 2 * NB] = kp;
+      }
+    } else if (role == 1) {
+      // ------------------------------ role U ------------------------------
+      float2 a1[NBP], fu[NBP], uu[C::NT2 > 0 ? C::NT2 : 1];
+      float ud[C::ND > 0 ? C::ND : 1];
+      float2 nkf[NBP], nku[NBP];
+      float2 hp[NBP], hc[NBP];
+#pragma unroll
+      for (int m = 0; m < NBP; ++m)
+        a1[m] = fu[m] = nkf[m] = nku[m] = hp[m] = hc[m] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < C::NT2; ++i) uu[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < C::ND; ++i) ud[i] = 0.f;
+      for (int u = 0; u < 16 / C::PAIRS; ++u) {
+        const int s = g % S;
+        tma::mbar_wait(&full[s], (g / S) & 1);
+        const float* slot = ring + (size_t)s * C::SLOT;
+        const int rb = i0 + C::PAIRS * u - 1;  // MS row of the stage box's first row
+#pragma unroll
+        for (int h = 0; h < C::PAIRS; ++h) {
+        const int t = C::PAIRS * u + h;
+        // horizontal bilinear of MS row gr (clamped) of band k at this lane's column
+        auto hrow = [&](int k, int gr) {
+          const float* r = slot + C::MSOFF +
+                           (k * C::MSR + (min(max(gr, 0), a.Hh - 1) - rb)) * kQ2Msw;
+          return fmaf(r[rx1] - r[rx0], hfx, r[rx0]);
+        };
+        if (t == 0) {
+#pragma unroll
+          for (int m = 0; m < NBP; ++m) {
+            const int k0 = 2 * m, k1 = 2 * m + 1 < NB ? 2 * m + 1 : 2 * m;
+            hp[m] = make_float2(hrow(k0, i0 - 1), hrow(k1, i0 - 1));
+            hc[m] = make_float2(hrow(k0, i0), hrow(k1, i0));
+          }
+        }
+        float2 hn[NBP];
+#pragma unroll
+        for (int m = 0; m < NBP; ++m) {
+          const int k0 = 2 * m, k1 = 2 * m + 1 < NB ? 2 * m + 1 : 2 * m;
+          hn[m] = make_float2(hrow(k0, i0 + t + 1), hrow(k1, i0 + t + 1));
+        }
+        float fv[2][NBE];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+#pragma unroll
+          for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
+        }
+        if (h == C::PAIRS - 1) {
+          __syncwarp();
+          if (lane == 0) tma::mbar_arrive(&empty[s]);
+          ++g;
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          float2 u[NBP];
+#pragma unroll
+          for (int m = 0; m < NBP; ++m) {
+            // row 2i: (i-1, i) fy 0.75; row 2i+1: (i, i+1) fy 0.25 (same
+            // fmaf(b - a, f, a) as above, lane-wise in pairs)
+            const float2 lo = p == 0 ? hp[m] : hc[m], hi = p == 0 ? hc[m] : hn[m];
+            const float fy = p == 0 ? 0.75f : 0.25f;
+            u[m] = __ffma2_rn(__fadd2_rn(hi, make_float2(-lo.x, -lo.y)), make_float2(fy, fy), lo);
+          }
+          if (t == 0 && p == 0) {
+#pragma unroll
+            for (int m = 0; m < NBP; ++m) {
+              nkf[m] = make_float2(-__shfl_sync(0xffffffffu, fv[0][2 * m], 0),
+                                   -__shfl_sync(0xffffffffu, fv[0][2 * m + 1], 0));
+              nku[m] = make_float2(-__shfl_sync(0xffffffffu, u[m].x, 0),
+                                   -__shfl_sync(0xffffffffu, u[m].y, 0));
+            }
+          }
+          float2 du[NBP];
+#pragma unroll
+          for (int m = 0; m < NBP; ++m) {
+            const float2 df = __fadd2_rn(make_float2(fv[p][2 * m], fv[p][2 * m + 1]), nkf[m]);
+            du[m] = __fadd2_rn(u[m], nku[m]);
+            a1[m] = __fadd2_rn(a1[m], du[m]);
+            fu[m] = __ffma2_rn(df, du[m], fu[m]);
+          }
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            const float dk = (k & 1) ? du[k >> 1].y : du[k >> 1].x;
+            if (k & 1) ud[k >> 1] = fmaf(dk, dk, ud[k >> 1]);
+#pragma unroll
+            for (int q = 0; q < C::npairs(k); ++q)
+              uu[C::base(k) + q] =
+                  __ffma2_rn(make_float2(dk, dk), du[(C::start(k) >> 1) + q], uu[C::base(k) + q]);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < NBP; ++m) {
+          hp[m] = hc[m];
+          hc[m] = hn[m];
+        }
+        }
+      }
+      // [U_k, UU tri, FU_k]
+      constexpr int NR = NB + L::NFF + NB;
+      float v[NR];
+      {
+        int r = 0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? a1[k >> 1].y : a1[k >> 1].x;
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) {
+            const int o = l - C::start(k);
+            v[r++] = ((k & 1) && l == k) ? ud[k >> 1]
+                                         : ((o & 1) ? uu[C::base(k) + (o >> 1)].y
+                                                    : uu[C::base(k) + (o >> 1)].x);
+          }
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fu[k >> 1].y : fu[k >> 1].x;
+      }
+      q2_reduce<NR>(tr, ds, lane, v, [&](int r) -> int {
+        if (r < NB) return NB + r;                         // S1 U_k
+        r -= NB;
+        if (r < L::NFF) return L::NP + L::NFF + r;         // S2 UU tri
+        return L::NP + 2 * L::NFF + (r - L::NFF);          // S2 FU
+      });
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) ds[L::NV + NB + k] = -((k & 1) ? nku[k >> 1].y : nku[k >> 1].x);
+      }
+    } else {
+      // ------------------------------ role L ------------------------------
+      float km[NB], kph, kpl;
+      shift_pan(praw_next, kph, kpl);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) km[k] = km_next[k];
+      // own bands: local m < H
+      float kml[H], rawc[H];
+      int foff[NBE], moff[H];
+#pragma unroll
+      for (int m = 0; m < NBE; ++m) {
+        const int b = band_of(m);
+        foff[m] = (b < NB ? b : NB) * C::PLANE;  // padding bands read the PAN row
+      }
+#pragma unroll
+      for (int m = 0; m < H; ++m) {
+        const int b = band_of(m);
+        float v = 0.f;
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+          if (b == k) v = km[k];
+        kml[m] = v;
+        moff[m] = (b < NB ? b : 0) * C::MSR * kQ2Msw + rxr;
+        rawc[m] = 0.f;
+      }
+      float lw1[H], lw2[H], lw3[H], sse[H], summ[H];
+      float lwp = 0.f, lwpp = 0.f;
+#pragma unroll
+      for (int m = 0; m < H; ++m) lw1[m] = lw2[m] = lw3[m] = sse[m] = summ[m] = 0.f;
+      for (int u = 0; u < 16 / C::PAIRS; ++u) {
+        const int s = g % S;
+        if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
+        tma::mbar_wait(&full[s], (g / S) & 1);
+        const float* slot = ring + (size_t)s * C::SLOT;
+#pragma unroll
+        for (int h = 0; h < C::PAIRS; ++h) {
+        const int t = C::PAIRS * u + h;
+        // M_k(i, x/2) of the own bands, i = i0 + t (box row 1 + h; i <= Hh - 1)
+        const float* msr = slot + C::MSOFF + (min(i0 + t, a.Hh - 1) - (i0 + t - h - 1)) * kQ2Msw;
+#pragma unroll
+        for (int m = 0; m < H; ++m) rawc[m] = msr[moff[m]];
+        float fv[2][NBE], pv[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+#pragma unroll
+          for (int m = 0; m < NBE; ++m) fv[p][m] = row[foff[m]];
+          pv[p] = row[NB * C::PLANE];
+        }
+        if (h == C::PAIRS - 1) {
+          __syncwarp();
+          if (lane == 0) tma::mbar_arrive(&empty[s]);
+          ++g;
+        }
+
+        // PAN cell: the exact (hi, lo) of the 4-pixel sum (both lanes agree)
+        float sp, tp, S_, T_;
+        two_sum(pv[0], pv[1], sp, tp);
+        two_sum(sp, __shfl_xor_sync(0xffffffffu, sp, 1), S_, T_);
+        const float plo = T_ + (tp + __shfl_xor_sync(0xffffffffu, tp, 1));
+        const float dpd = 0.25f * ((S_ - kph) + (plo - kpl));
+        lwp += dpd;
+        lwpp = fmaf(dpd, dpd, lwpp);
+        // per-column vertical TwoSums of every band, then the partner's
+        // columns for this lane's own bands (local m < H)
+        float sv[NBE], tv[NBE];
+#pragma unroll
+        for (int m = 0; m < NBE; ++m) two_sum(fv[0][m], fv[1][m], sv[m], tv[m]);
+#pragma unroll
+        for (int m = 0; m < H; ++m) {
+          const float so = __shfl_xor_sync(0xffffffffu, sv[H + m], 1);
+          const float to = __shfl_xor_sync(0xffffffffu, tv[H + m], 1);
+          float Sc, Tc;
+          two_sum(sv[m], so, Sc, Tc);
+          const float lo = Tc + (tv[m] + to);
+          const float e = fmaf(Sc, 0.25f, -rawc[m]) + 0.25f * lo;
+          sse[m] = fmaf(e, e, sse[m]);
+          summ[m] += rawc[m];
+          const float dm = rawc[m] - kml[m];
+          lw1[m] += dm;
+          lw2[m] = fmaf(dm, dm, lw2[m]);
+          lw3[m] = fmaf(dm, dpd, lw3[m]);
+        }
+        }
+      }
+      // low-res + ERGAS layout (as above): [S1m[NB] S1p S2mm[NB] S2pp S2mp[NB]]
+      // then [sse[NB] summ[NB]]; band b's value comes from the lanes owning it
+      // (even lanes: b < H, odd lanes: b >= H); PAN terms from even lanes
+      constexpr int NR = L::NLOW + L::NERG;
+      float v[NR];
+      {
+        // band b's value comes from the lanes owning it (even: b < H, odd:
+        // b >= H); the PAN terms from the even lanes
+        auto own = [&](int b, const float (&w)[H]) -> float {
+          return ((b >= H) == odd) ? w[b < H ? b : b - H] : 0.f;
+        };
+        int r = 0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = own(k, lw1);
+        v[r++] = odd ? 0.f : lwp;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = own(k, lw2);
+        v[r++] = odd ? 0.f : lwpp;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = own(k, lw3);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = own(k, sse);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = own(k, summ);
+      }
+      q2_reduce<NR>(tr, ds + L::NT, lane, v, [](int r) -> int { return r; });
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) ds[L::NV + L::NP + k] = km[k];
+      }
+      __syncwarp();
+      if (low_ok) {
+        const double* lowv = ds + L::NT;
+        const size_t nlow = (size_t)a.nbr_l * a.nbc_l;
+        double* dst = part_low + (size_t)((br & 1) * 2 + (bc & 1)) * (L::NLOW + NB + 1) * nlow +
+                      (size_t)(lr * a.nbc_l + lc);
+        for (int k = lane; k < L::NLOW; k += 32) dst[k * nlow] = lowv[k];
+        if (lane < NB) dst[(L::NLOW + lane) * nlow] = ds[L::NV + L::NP + lane];
+        if (lane == 0) dst[(L::NLOW + NB) * nlow] = (double)kph * 0.25 + (double)kpl * 0.25;
+      }
+      double* ewp = ew + (size_t)(parity * kQ2Bc + bcl) * L::NERG;
+      for (int k = lane; k < L::NERG; k += 32) ewp[k] = blk_ok ? ds[L::NT + L::NLOW + k] : 0.0;
+    }
+
+    // the three warps of this block column meet; role F scores its Q pairs
+    asm volatile("bar.sync %0, 96;" ::"r"(2 + bcl) : "memory");
+    if (role == 0) {
+      double* myq = qw + (size_t)(parity * kQ2Bc + bcl) * L::NQ;
+      constexpr int CP = NB * (NB - 1) / 2;
+      for (int q = lane; q < L::NQ; q += 32) {
+        int pa, pb, saa, sbb, sab;
+        if (q < NB) {
+          pa = q;
+          pb = NB + q;
+          saa = L::tri(q, q);
+          sbb = L::NFF + L::tri(q, q);
+          sab = 2 * L::NFF + q;
+        } else if (q < NB + 2 * CP) {
+          int p = (q - NB) % CP, k = 0;
+          const int off = (q - NB) < CP ? 0 : 1;
+          while (p >= NB - 1 - k) {
+            p -= NB - 1 - k;
+            ++k;
+          }
+          const int l = k + 1 + p;
+          pa = off * NB + k;
+          pb = off * NB + l;
+          saa = off * L::NFF + L::tri(k, k);
+          sbb = off * L::NFF + L::tri(l, l);
+          sab = off * L::NFF + L::tri(k, l);
+        } else {
+          const int k = q - NB - 2 * CP;
+          pa = k;
+          pb = 2 * NB;
+          saa = L::tri(k, k);
+          sbb = 2 * L::NFF + 2 * NB;
+          sab = 2 * L::NFF + NB + k;
+        }
+        myq[q] = blk_ok ? q_from_sums(1024.0, ds[L::NV + pa], ds[L::NV + pb], ds[pa], ds[pb],
+                                      ds[L::NP + saa], ds[L::NP + sbb], ds[L::NP + sab],
+                                      undecidable)
+                        : 0.0;
+      }
+    }
+    // tile-level deterministic sums over the block columns (consumers only;
+    // the parity buffers keep the next tile off the ones being read)
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kQ2Cons) : "memory");
+    if (warp == 0) {
+      const double* qwp = qw + (size_t)parity * kQ2Bc * L::NQ;
+      const double* ewp = ew + (size_t)parity * kQ2Bc * L::NERG;
+      for (int q = lane; q < L::NQ; q += 32) {
+        double v = 0.0;
+        for (int w = 0; w < kQ2Bc; ++w) v += qwp[w * L::NQ + q];
+        part_q[(size_t)q * ntiles + tile] = v;
+      }
+      for (int q = lane; q < L::NERG; q += 32) {
+        double v = 0.0;
+        for (int w = 0; w < kQ2Bc; ++w) v += ewp[w * L::NERG + q];
+        part_erg[(size_t)q * ntiles + tile] = v;
+      }
+    }
+  }
+}
+
 // ---- host side ---------------------------------------------------------------
 constexpr int kEdgeCtas = 256;
 
@@ -632,19 +1280,72 @@ static size_t qs_smem() {
          (size_t)kQsWarps * L::NT * kTrPad * sizeof(float) + 16;
 }
 
-void qs_geometry(int h, int w, int& nbr, int& nbc, int& nbr_l, int& nbc_l, int& ncx) {
+// Which scene kernel runs: the role-split one (default) or, with
+// WF_QNR_KERNEL=v1, the one-warp-per-block one (kept for A/B timing).
+static bool qs_use_v1() {
+  const char* e = getenv("WF_QNR_KERNEL");
+  return e && e[0] == 'v' && e[1] == '1';
+}
+
+template <int NB>
+static size_t q2_smem() {
+  using L = QsLayout<NB>;
+  using C = Q2Cfg<NB>;
+  return 128 + (size_t)C::S * C::SLOT * sizeof(float) + 2 * C::S * sizeof(uint64_t) +
+         (size_t)2 * kQ2Bc * (L::NQ + L::NERG + C::DS) * sizeof(double) +
+         (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float) + 16;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 2-D float32 tensor map of a rows x cols plane (pitch in elements), box
+// box_cols x box_rows, zero fill outside
+static bool plane_map(CUtensorMap* m, const float* base, long long pitch, int rows, int cols,
+                      int box_cols, int box_rows) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void qs_geometry(int h, int w, int& nbr, int& nbc, int& nbr_l, int& nbc_l, int& ncx,
+                 int bc_per_cta) {
   nbr = h / 32;
   nbc = w / 32;
   nbr_l = (h / 2) / 32;
   nbc_l = (w / 2) / 32;
-  ncx = (nbc + kQsWarps - 1) / kQsWarps;
+  ncx = (nbc + bc_per_cta - 1) / bc_per_cta;
 }
 
 template <int NB>
 static size_t qs_workspace_nb(int h, int w) {
   using L = QsLayout<NB>;
   int nbr, nbc, nbr_l, nbc_l, ncx;
-  qs_geometry(h, w, nbr, nbc, nbr_l, nbc_l, ncx);
+  // sized for the narrower tiles of the two kernels (more tiles)
+  qs_geometry(h, w, nbr, nbc, nbr_l, nbc_l, ncx, kQ2Bc < kQsWarps ? kQ2Bc : kQsWarps);
   const size_t ncta = (size_t)nbr * ncx;
   return sizeof(double) * (ncta * L::NQ + (size_t)nbr_l * nbc_l * 4 * (L::NLOW + NB + 1) +
                            ncta * L::NERG + (size_t)kEdgeCtas * 2 * NB) +
@@ -682,16 +1383,31 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   a.W = w;
   a.Hh = h / 2;
   a.Wh = w / 2;
-  qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, a.ncx);
+  const bool v1 = qs_use_v1();
+  qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, a.ncx, v1 ? kQsWarps : kQ2Bc);
   const int ncta = a.nbr * a.ncx;
   double* part_q = static_cast<double*>(workspace);
   double* part_low = part_q + (size_t)ncta * L::NQ;
   double* part_erg = part_low + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
   double* part_edge = part_erg + (size_t)ncta * L::NERG;
-  const size_t smem = qs_smem<NB>();
-  auto kern = quality_scene_kernel<NB>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  Q2Maps maps;
+  bool use_v1 = v1;
+  if (!use_v1) {
+    // the role-split kernel needs tensor maps; 16-byte strides (W % 4 == 0)
+    bool ok = (fp % 4 == 0) && (mp % 4 == 0) && (pp % 4 == 0);
+    for (int k = 0; ok && k < NB; ++k)
+      ok = plane_map(&maps.f[k], F[k], fp, h, w, kQ2Cols, 2 * Q2Cfg<NB>::PAIRS) &&
+           plane_map(&maps.m[k], M[k], mp, h / 2, w / 2, kQ2Msw, Q2Cfg<NB>::MSR);
+    ok = ok && plane_map(&maps.p, P, pp, h, w, kQ2Cols, 2 * Q2Cfg<NB>::PAIRS);
+    if (!ok) return cudaErrorInvalidValue;
+  }
+  const size_t smem = use_v1 ? qs_smem<NB>() : q2_smem<NB>();
+  cudaError_t e = use_v1 ? cudaFuncSetAttribute(quality_scene_kernel<NB>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem)
+                         : cudaFuncSetAttribute(quality_split_kernel<NB>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(undecidable, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
@@ -699,7 +1415,12 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = ncta < sms ? ncta : sms;  // persistent: one CTA per SM
-  kern<<<grid, 32 * (kQsWarps + 1), smem, s>>>(a, part_q, part_low, part_erg, undecidable);
+  if (use_v1)
+    quality_scene_kernel<NB><<<grid, 32 * (kQsWarps + 1), smem, s>>>(a, part_q, part_low,
+                                                                      part_erg, undecidable);
+  else
+    quality_split_kernel<NB><<<grid, kQ2Threads, smem, s>>>(a, maps, part_q, part_low, part_erg,
+                                                            undecidable);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int row_lo = 16 * a.nbr, col_lo = 16 * a.nbc;
   int nedge = 0;

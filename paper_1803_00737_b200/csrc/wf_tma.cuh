@@ -61,5 +61,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// One 2-D tensor-map copy (UTMALDG): the box at (c0 = column, c1 = row) of
+// the tensor `tmap` describes (a __grid_constant__ CUtensorMap) lands densely
+// at dst (128-byte aligned); out-of-range elements are zero-filled and still
+// count towards the transaction bytes.
+__device__ __forceinline__ void tensor_g2s_2d(void* dst, const void* tmap, int c0, int c1,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 }  // namespace tma
 }  // namespace wf
