@@ -739,15 +739,17 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
   using C = Q2Cfg<NB>;
   constexpr int S = C::S, NBE = C::NBE, H = C::H, NBP = C::NBP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* ring = reinterpret_cast<float*>(  // tensor-copy destinations: 128-byte aligned
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // tensor-copy destinations 128-byte aligned; the offset is added to
+  // smem_raw itself so the compiler keeps the pointers in the shared window
+  // (LDS, not generic LD)
+  float* ring = reinterpret_cast<float*>(
+      smem_raw + ((128u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 127u)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * C::SLOT);
   uint64_t* empty = full + S;
   double* qw = reinterpret_cast<double*>(empty + S);  // [2][kQ2Bc][NQ]
   double* ew = qw + 2 * kQ2Bc * L::NQ;                 // [2][kQ2Bc][NERG]
   double* dsb = ew + 2 * kQ2Bc * L::NERG;              // [2][kQ2Bc][DS]
-  float* trs = reinterpret_cast<float*>(                // [kQ2Cons][kQ2TrRows][kTrPad]
-      (reinterpret_cast<uintptr_t>(dsb + 2 * kQ2Bc * C::DS) + 15) & ~uintptr_t(15));
+  float* trs = reinterpret_cast<float*>(dsb + 2 * kQ2Bc * C::DS);  // [kQ2Cons][kQ2TrRows][kTrPad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.nbr * a.ncx;
@@ -772,7 +774,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       const int ms0 = max((col0 >> 1) - 4, 0);
       for (int u = 0; u < 16 / C::PAIRS; ++u, ++g) {
         const int s = g % S, r = g / S;
-        if (r > 0 && lane == 0) tma::mbar_wait(&empty[s], (r - 1) & 1);
+        if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
         __syncwarp();
         if (lane == 0) tma::mbar_arrive_expect_tx(&full[s], kStageBytes);
         __syncwarp();
@@ -866,7 +868,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int i = 0; i < C::ND; ++i) fd[i] = 0.f;
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
-        tma::mbar_wait(&full[s], (g / S) & 1);
+        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll
         for (int h = 0; h < C::PAIRS; ++h) {  // row pair h of the stage
@@ -967,7 +969,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int i = 0; i < C::ND; ++i) ud[i] = 0.f;
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
-        tma::mbar_wait(&full[s], (g / S) & 1);
+        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
         const int rb = i0 + C::PAIRS * u - 1;  // MS row of the stage box's first row
 #pragma unroll
@@ -1111,7 +1113,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
         if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
-        tma::mbar_wait(&full[s], (g / S) & 1);
+        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll
         for (int h = 0; h < C::PAIRS; ++h) {
