@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
     const int mlcol = wrap((base >> 1) - HALO, Wh);
     for (int n = 0; n < nloads; ++n) {
       const int s = n % S, r = n / S;
-      if (r > 0 && lane == 0) tma::mbar_wait(&empty[s], (r - 1) & 1);
+      if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
       __syncwarp();
       const bool with_ms = n >= 1;
       if (lane == 0)
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
 
   for (int n = 0; n < nloads; ++n) {
     const int s = n % S;
-    tma::mbar_wait(&full[s], (n / S) & 1);
+    tma::mbar_wait_sleep(&full[s], (n / S) & 1);
     const T* slot = slots + (size_t)s * SLOT;
     Acc v[2][8];  // PAN cols c-2 .. c+5 of the slot's two rows
 #pragma unroll

@@ -746,9 +746,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       smem_raw + ((128u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 127u)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * C::SLOT);
   uint64_t* empty = full + S;
-  double* qw = reinterpret_cast<double*>(empty + S);  // [2][kQ2Bc][NQ]
-  double* ew = qw + 2 * kQ2Bc * L::NQ;                 // [2][kQ2Bc][NERG]
-  double* dsb = ew + 2 * kQ2Bc * L::NERG;              // [2][kQ2Bc][DS]
+  double* dsb = reinterpret_cast<double*>(empty + S);  // [2][kQ2Bc][DS]
   float* trs = reinterpret_cast<float*>(dsb + 2 * kQ2Bc * C::DS);  // [kQ2Cons][kQ2TrRows][kTrPad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1206,14 +1204,16 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         if (lane < NB) dst[(L::NLOW + lane) * nlow] = ds[L::NV + L::NP + lane];
         if (lane == 0) dst[(L::NLOW + NB) * nlow] = (double)kph * 0.25 + (double)kpl * 0.25;
       }
-      double* ewp = ew + (size_t)(parity * kQ2Bc + bcl) * L::NERG;
-      for (int k = lane; k < L::NERG; k += 32) ewp[k] = blk_ok ? ds[L::NT + L::NLOW + k] : 0.0;
+      // per-block ERGAS partials, quantity-major (one per block column of a tile)
+      const size_t nparts = (size_t)ntiles * kQ2Bc, part = (size_t)tile * kQ2Bc + bcl;
+      for (int k = lane; k < L::NERG; k += 32)
+        part_erg[k * nparts + part] = blk_ok ? ds[L::NT + L::NLOW + k] : 0.0;
     }
 
     // the three warps of this block column meet; role F scores its Q pairs
     asm volatile("bar.sync %0, 96;" ::"r"(2 + bcl) : "memory");
     if (role == 0) {
-      double* myq = qw + (size_t)(parity * kQ2Bc + bcl) * L::NQ;
+      const size_t nparts = (size_t)ntiles * kQ2Bc, part = (size_t)tile * kQ2Bc + bcl;
       constexpr int CP = NB * (NB - 1) / 2;
       for (int q = lane; q < L::NQ; q += 32) {
         int pa, pb, saa, sbb, sab;
@@ -1244,29 +1244,15 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
           sbb = 2 * L::NFF + 2 * NB;
           sab = 2 * L::NFF + NB + k;
         }
-        myq[q] = blk_ok ? q_from_sums(1024.0, ds[L::NV + pa], ds[L::NV + pb], ds[pa], ds[pb],
-                                      ds[L::NP + saa], ds[L::NP + sbb], ds[L::NP + sab],
-                                      undecidable)
-                        : 0.0;
+        part_q[q * nparts + part] =
+            blk_ok ? q_from_sums(1024.0, ds[L::NV + pa], ds[L::NV + pb], ds[pa], ds[pb],
+                                 ds[L::NP + saa], ds[L::NP + sbb], ds[L::NP + sab], undecidable)
+                   : 0.0;
       }
     }
-    // tile-level deterministic sums over the block columns (consumers only;
-    // the parity buffers keep the next tile off the ones being read)
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kQ2Cons) : "memory");
-    if (warp == 0) {
-      const double* qwp = qw + (size_t)parity * kQ2Bc * L::NQ;
-      const double* ewp = ew + (size_t)parity * kQ2Bc * L::NERG;
-      for (int q = lane; q < L::NQ; q += 32) {
-        double v = 0.0;
-        for (int w = 0; w < kQ2Bc; ++w) v += qwp[w * L::NQ + q];
-        part_q[(size_t)q * ntiles + tile] = v;
-      }
-      for (int q = lane; q < L::NERG; q += 32) {
-        double v = 0.0;
-        for (int w = 0; w < kQ2Bc; ++w) v += ewp[w * L::NERG + q];
-        part_erg[(size_t)q * ntiles + tile] = v;
-      }
-    }
+    // (ds is double-buffered by tile parity: a block column's warps can only
+    // reach this tile's successor-but-one after the ring has moved past it,
+    // i.e. after role F has scored this tile)
   }
 }
 
@@ -1294,7 +1280,7 @@ static size_t q2_smem() {
   using L = QsLayout<NB>;
   using C = Q2Cfg<NB>;
   return 128 + (size_t)C::S * C::SLOT * sizeof(float) + 2 * C::S * sizeof(uint64_t) +
-         (size_t)2 * kQ2Bc * (L::NQ + L::NERG + C::DS) * sizeof(double) +
+         (size_t)2 * kQ2Bc * C::DS * sizeof(double) +
          (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float) + 16;
 }
 
@@ -1348,7 +1334,8 @@ static size_t qs_workspace_nb(int h, int w) {
   int nbr, nbc, nbr_l, nbc_l, ncx;
   // sized for the narrower tiles of the two kernels (more tiles)
   qs_geometry(h, w, nbr, nbc, nbr_l, nbc_l, ncx, kQ2Bc < kQsWarps ? kQ2Bc : kQsWarps);
-  const size_t ncta = (size_t)nbr * ncx;
+  // v2 writes one partial per block column of a tile (>= v1's one per tile)
+  const size_t ncta = (size_t)nbr * ncx * kQ2Bc;
   return sizeof(double) * (ncta * L::NQ + (size_t)nbr_l * nbc_l * 4 * (L::NLOW + NB + 1) +
                            ncta * L::NERG + (size_t)kEdgeCtas * 2 * NB) +
          64;
@@ -1387,11 +1374,12 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   a.Wh = w / 2;
   const bool v1 = qs_use_v1();
   qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, a.ncx, v1 ? kQsWarps : kQ2Bc);
-  const int ncta = a.nbr * a.ncx;
+  const int ncta = a.nbr * a.ncx;  // tiles
+  const int nparts = v1 ? ncta : ncta * kQ2Bc;  // Q / ERGAS partials
   double* part_q = static_cast<double*>(workspace);
-  double* part_low = part_q + (size_t)ncta * L::NQ;
+  double* part_low = part_q + (size_t)nparts * L::NQ;
   double* part_erg = part_low + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
-  double* part_edge = part_erg + (size_t)ncta * L::NERG;
+  double* part_edge = part_erg + (size_t)nparts * L::NERG;
   Q2Maps maps;
   bool use_v1 = v1;
   if (!use_v1) {
@@ -1431,7 +1419,7 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
     quality_edge_kernel<NB><<<nedge, 256, 0, s>>>(a, row_lo, col_lo, part_edge);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  quality_finish_kernel<NB><<<L::NQ + 3 * NB, 1024, 0, s>>>(a, part_q, ncta, part_low, part_erg,
+  quality_finish_kernel<NB><<<L::NQ + 3 * NB, 1024, 0, s>>>(a, part_q, nparts, part_low, part_erg,
                                                             part_edge, nedge, out, undecidable);
   return cudaGetLastError();
 }
