@@ -113,6 +113,14 @@ __device__ __forceinline__ void two_sum(float a, float b, float& s, float& t) {
   t = (a - (s - bb)) + (b - bb);
 }
 
+// TwoSum on two lanes at once (FADD2 rounds each lane like FADD)
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ void two_sum2(float2 a, float2 b, float2& s, float2& t) {
+  s = __fadd2_rn(a, b);
+  const float2 bb = __fadd2_rn(s, neg2(a));
+  t = __fadd2_rn(__fadd2_rn(a, neg2(__fadd2_rn(s, neg2(bb)))), __fadd2_rn(b, neg2(bb)));
+}
+
 // The degraded-PAN shift of a low-res block as the exact float pair (hi, lo)
 // of its 2x2 sum (p00 + p10, p01 + p11 by TwoSum, then across), formed by the
 // same TwoSum sequence the main loops use, so a constant region gives exactly
@@ -1085,29 +1093,35 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       shift_pan(praw_next, kph, kpl);
 #pragma unroll
       for (int k = 0; k < NB; ++k) km[k] = km_next[k];
-      // own bands: local m < H
-      float kml[H], rawc[H];
-      int foff[NBE], moff[H];
+      // own bands: local m < H, processed as float2 pairs (2j, 2j + 1); the
+      // pair lane past H is padding (never reported)
+      constexpr int HP = (H + 1) / 2;
+      float2 kml[HP];
+      int foff[NBE], moff[2 * HP];
 #pragma unroll
       for (int m = 0; m < NBE; ++m) {
         const int b = band_of(m);
         foff[m] = (b < NB ? b : NB) * C::PLANE;  // padding bands read the PAN row
       }
 #pragma unroll
-      for (int m = 0; m < H; ++m) {
-        const int b = band_of(m);
+      for (int m = 0; m < 2 * HP; ++m) {
+        const int b = m < H ? band_of(m) : NB;
         float v = 0.f;
 #pragma unroll
         for (int k = 0; k < NB; ++k)
           if (b == k) v = km[k];
-        kml[m] = v;
+        if (m & 1)
+          kml[m >> 1].y = v;
+        else
+          kml[m >> 1].x = v;
         moff[m] = (b < NB ? b : 0) * C::MSR * kQ2Msw + rxr;
-        rawc[m] = 0.f;
       }
-      float lw1[H], lw2[H], lw3[H], sse[H], summ[H];
+      float2 lw1[HP], lw2[HP], lw3[HP], sse[HP], summ[HP];
       float lwp = 0.f, lwpp = 0.f;
 #pragma unroll
-      for (int m = 0; m < H; ++m) lw1[m] = lw2[m] = lw3[m] = sse[m] = summ[m] = 0.f;
+      for (int j = 0; j < HP; ++j)
+        lw1[j] = lw2[j] = lw3[j] = sse[j] = summ[j] = make_float2(0.f, 0.f);
+      const float2 q25 = make_float2(0.25f, 0.25f);
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
         if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
@@ -1118,8 +1132,9 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const int t = C::PAIRS * u + h;
         // M_k(i, x/2) of the own bands, i = i0 + t (box row 1 + h; i <= Hh - 1)
         const float* msr = slot + C::MSOFF + (min(i0 + t, a.Hh - 1) - (i0 + t - h - 1)) * kQ2Msw;
+        float2 raw[HP];
 #pragma unroll
-        for (int m = 0; m < H; ++m) rawc[m] = msr[moff[m]];
+        for (int j = 0; j < HP; ++j) raw[j] = make_float2(msr[moff[2 * j]], msr[moff[2 * j + 1]]);
         float fv[2][NBE], pv[2];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
@@ -1142,38 +1157,50 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const float dpd = 0.25f * ((S_ - kph) + (plo - kpl));
         lwp += dpd;
         lwpp = fmaf(dpd, dpd, lwpp);
-        // per-column vertical TwoSums of every band, then the partner's
-        // columns for this lane's own bands (local m < H)
-        float sv[NBE], tv[NBE];
+        // per-column vertical TwoSums of every band (band pairs), then the
+        // partner's columns for this lane's own bands (local m < H)
+        float2 sv[NBE / 2], tv[NBE / 2];
 #pragma unroll
-        for (int m = 0; m < NBE; ++m) two_sum(fv[0][m], fv[1][m], sv[m], tv[m]);
+        for (int j = 0; j < NBE / 2; ++j)
+          two_sum2(make_float2(fv[0][2 * j], fv[0][2 * j + 1]),
+                   make_float2(fv[1][2 * j], fv[1][2 * j + 1]), sv[j], tv[j]);
+        auto lanev = [](const float2 (&v)[NBE / 2], int m) { return (m & 1) ? v[m >> 1].y : v[m >> 1].x; };
+        float so[2 * HP], to[2 * HP];
 #pragma unroll
-        for (int m = 0; m < H; ++m) {
-          const float so = __shfl_xor_sync(0xffffffffu, sv[H + m], 1);
-          const float to = __shfl_xor_sync(0xffffffffu, tv[H + m], 1);
-          float Sc, Tc;
-          two_sum(sv[m], so, Sc, Tc);
-          const float lo = Tc + (tv[m] + to);
-          const float e = fmaf(Sc, 0.25f, -rawc[m]) + 0.25f * lo;
-          sse[m] = fmaf(e, e, sse[m]);
-          summ[m] += rawc[m];
-          const float dm = rawc[m] - kml[m];
-          lw1[m] += dm;
-          lw2[m] = fmaf(dm, dm, lw2[m]);
-          lw3[m] = fmaf(dm, dpd, lw3[m]);
+        for (int m = 0; m < 2 * HP; ++m) {
+          so[m] = m < H ? __shfl_xor_sync(0xffffffffu, lanev(sv, H + m), 1) : 0.f;
+          to[m] = m < H ? __shfl_xor_sync(0xffffffffu, lanev(tv, H + m), 1) : 0.f;
+        }
+        const float2 dpd2 = make_float2(dpd, dpd);
+#pragma unroll
+        for (int j = 0; j < HP; ++j) {
+          const int m0 = 2 * j, m1 = 2 * j + 1;
+          const float2 own_s = make_float2(lanev(sv, m0), m1 < H ? lanev(sv, m1) : 0.f);
+          const float2 own_t = make_float2(lanev(tv, m0), m1 < H ? lanev(tv, m1) : 0.f);
+          float2 Sc, Tc;
+          two_sum2(own_s, make_float2(so[m0], so[m1]), Sc, Tc);
+          const float2 lo = __fadd2_rn(Tc, __fadd2_rn(own_t, make_float2(to[m0], to[m1])));
+          // e = (S/4 - m) + lo/4, the scalar form's exact operation order
+          const float2 e = __fadd2_rn(__ffma2_rn(Sc, q25, neg2(raw[j])), __fmul2_rn(q25, lo));
+          sse[j] = __ffma2_rn(e, e, sse[j]);
+          summ[j] = __fadd2_rn(summ[j], raw[j]);
+          const float2 dm = __fadd2_rn(raw[j], neg2(kml[j]));
+          lw1[j] = __fadd2_rn(lw1[j], dm);
+          lw2[j] = __ffma2_rn(dm, dm, lw2[j]);
+          lw3[j] = __ffma2_rn(dm, dpd2, lw3[j]);
         }
         }
       }
       // low-res + ERGAS layout (as above): [S1m[NB] S1p S2mm[NB] S2pp S2mp[NB]]
-      // then [sse[NB] summ[NB]]; band b's value comes from the lanes owning it
-      // (even lanes: b < H, odd lanes: b >= H); PAN terms from even lanes
+      // then [sse[NB] summ[NB]]
       constexpr int NR = L::NLOW + L::NERG;
       float v[NR];
       {
         // band b's value comes from the lanes owning it (even: b < H, odd:
         // b >= H); the PAN terms from the even lanes
-        auto own = [&](int b, const float (&w)[H]) -> float {
-          return ((b >= H) == odd) ? w[b < H ? b : b - H] : 0.f;
+        auto own = [&](int b, const float2 (&w)[HP]) -> float {
+          const int m = b < H ? b : b - H;
+          return ((b >= H) == odd) ? ((m & 1) ? w[m >> 1].y : w[m >> 1].x) : 0.f;
         };
         int r = 0;
 #pragma unroll
