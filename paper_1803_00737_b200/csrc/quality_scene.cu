@@ -671,8 +671,8 @@ constexpr int kQ2Prod = 1;               // producer warps
 constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
 constexpr int kQ2TrRows = 16;            // transpose chunk (rows of 32 lanes)
 
-#ifndef WF_Q2_STAGES
-#define WF_Q2_STAGES 2
+#ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound)
+#define WF_Q2_STAGES 3
 #endif
 // Tensor maps of the scene planes (2-D, float32): the producer moves a
 // 2-row x 160-column box of each PAN-resolution plane and one 96-column MS
@@ -685,7 +685,7 @@ struct Q2Maps {
 
 template <int NB>
 struct Q2Cfg {
-  static constexpr int S = WF_Q2_STAGES;
+  static constexpr int S = NB <= 6 ? WF_Q2_STAGES : 2;
   // A stage is PAIRS row pairs (8 PAN rows): plane q (F_0..F_{NB-1}, P) as a
   // dense [8][kQ2Cols] box at q * PLANE, then per band the MSR = 6 MS rows
   // i0 + 4u - 1 .. i0 + 4u + 4 the stage's bilinear and 2x2 cells touch
@@ -981,26 +981,27 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 #pragma unroll
         for (int h = 0; h < C::PAIRS; ++h) {
         const int t = C::PAIRS * u + h;
-        // horizontal bilinear of MS row gr (clamped) of band k at this lane's column
-        auto hrow = [&](int k, int gr) {
-          const float* r = slot + C::MSOFF +
-                           (k * C::MSR + (min(max(gr, 0), a.Hh - 1) - rb)) * kQ2Msw;
-          return fmaf(r[rx1] - r[rx0], hfx, r[rx0]);
+        // horizontal bilinear of MS row gr (clamped) of bands (2m, 2m + 1) at
+        // this lane's column: fmaf(r1 - r0, fx, r0) on both lanes
+        const float2 fx2 = make_float2(hfx, hfx);
+        auto hrow2 = [&](int m, int gr) {
+          const int k0 = 2 * m, k1 = 2 * m + 1 < NB ? 2 * m + 1 : 2 * m;
+          const float* r = slot + C::MSOFF + (min(max(gr, 0), a.Hh - 1) - rb) * kQ2Msw;
+          const float* ra = r + k0 * C::MSR * kQ2Msw;
+          const float* rb_ = r + k1 * C::MSR * kQ2Msw;
+          const float2 v0 = make_float2(ra[rx0], rb_[rx0]), v1 = make_float2(ra[rx1], rb_[rx1]);
+          return __ffma2_rn(__fadd2_rn(v1, neg2(v0)), fx2, v0);
         };
         if (t == 0) {
 #pragma unroll
           for (int m = 0; m < NBP; ++m) {
-            const int k0 = 2 * m, k1 = 2 * m + 1 < NB ? 2 * m + 1 : 2 * m;
-            hp[m] = make_float2(hrow(k0, i0 - 1), hrow(k1, i0 - 1));
-            hc[m] = make_float2(hrow(k0, i0), hrow(k1, i0));
+            hp[m] = hrow2(m, i0 - 1);
+            hc[m] = hrow2(m, i0);
           }
         }
         float2 hn[NBP];
 #pragma unroll
-        for (int m = 0; m < NBP; ++m) {
-          const int k0 = 2 * m, k1 = 2 * m + 1 < NB ? 2 * m + 1 : 2 * m;
-          hn[m] = make_float2(hrow(k0, i0 + t + 1), hrow(k1, i0 + t + 1));
-        }
+        for (int m = 0; m < NBP; ++m) hn[m] = hrow2(m, i0 + t + 1);
         float fv[2][NBE];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
