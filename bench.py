@@ -344,7 +344,8 @@ def measure_quality(scene, steps, warmup, peak):
         "report": {"ergas": rep.ergas, "qnr": rep.qnr, "d_lambda": rep.d_lambda, "d_s": rep.d_s},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "algorithmic_bytes_per_report": nbytes,
-                     "kernels": "quality_scene_kernel<6> + quality_edge_kernel + quality_finish"},
+                     "traffic": ncu_traffic("quality_split_kernel_6"),
+                     "kernels": "quality_split_kernel<6> (F / U / 2x2-cell warp roles, tensor-map stages) + quality_edge_kernel + quality_finish_kernel"},
         "reference_cpu_estimate": "qnr() at 4096^2 x 6 bands: 47 s single-thread (SURVEY.md S5)",
     }
 
@@ -404,6 +405,8 @@ def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_launch": nbytes,
+                         "traffic": ncu_traffic("fuse_haar_u8_kernel_6" if kind is WaveletKind.HAAR
+                                                else "fuse_d4_tma_kernel_unsigned_char__6__4"),
                          "kernel": ("fuse_haar_u8_kernel<B=6> (16-bit lanes)"
                                     if kind is WaveletKind.HAAR
                                     else "fuse_d4_tma_kernel<u8,B=6,4 consumer warps>")},
