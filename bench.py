@@ -339,6 +339,28 @@ def measure_quality(scene, steps, warmup, peak):
     rep = wf.qnr(scene.out, scene.ms, scene.pan)
     nbytes = (4 * nb + 4) * h * w + nb * (h // 2) * (w // 2) * 4
     achieved = nbytes / (per * 1e-3) / 1e9
+
+    # Haar fusion + the same report in ONE pass
+    # (wf_fuse_quality_f32): the fused bands are written, never re-read --
+    # reported next to fuse() + qnr() because it is the slower of the two
+    fo = [torch.empty_like(scene.pan) for _ in scene.ms]
+    fop = _native.ptr_array([t.data_ptr() for t in fo])
+
+    def run_fused():
+        _native.check(lib.wf_fuse_quality_f32(1, scene.pan.data_ptr(), w, mp, w // 2, fop, w, nb,
+                                              h, w, ws.data_ptr(), out.data_ptr(),
+                                              flag.data_ptr(), _device.stream_ptr()))
+
+    for _ in range(warmup):
+        run_fused()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(n):
+        run_fused()
+    e1.record()
+    torch.cuda.synchronize()
+    per_fused = e0.elapsed_time(e1) / n
+    same = all(torch.equal(a_, b_) for a_, b_ in zip(fo, scene.out))
     return {
         "ms_per_report": round(per, 4),
         "report": {"ergas": rep.ergas, "qnr": rep.qnr, "d_lambda": rep.d_lambda, "d_s": rep.d_s},
@@ -347,7 +369,32 @@ def measure_quality(scene, steps, warmup, peak):
                      "traffic": ncu_traffic("quality_split_kernel_6"),
                      "kernels": "quality_split_kernel<6> (F / U / 2x2-cell warp roles, tensor-map stages) + quality_edge_kernel + quality_finish_kernel"},
         "reference_cpu_estimate": "qnr() at 4096^2 x 6 bands: 47 s single-thread (SURVEY.md S5)",
+        "fused_haar_fuse_and_report": {
+            "ms_per_scene": round(per_fused, 4),
+            "vs_separate_ms": round(per + hmean_fuse_ms(scene), 4),
+            "fused_bands_identical_to_fuse": same,
+            "api": "wf_fuse_quality_f32 / paper_1803_00737_b200.fuse_and_qnr(one_pass=True)",
+        },
     }
+
+
+def hmean_fuse_ms(scene, reps=10):
+    """CUDA-event time of one whole-scene Haar fusion launch (for the
+    fused-vs-separate comparison)."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind
+
+    run = scene.launcher(WaveletKind.HAAR)
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):

@@ -252,6 +252,15 @@ int64_t wf_quality_scene_workspace_bytes(int nbands, int h, int w);
 int wf_quality_scene_f32(const float* const* fused, const float* const* ms, const float* pan,
                          int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
                          int w, void* workspace, double* out, int* undecidable, void* stream);
+/* SURVEY.md 8(f) row f1, second half: Haar fusion and its quality report in
+ * ONE pass over the scene -- fusion.py:153-183 fuse(pan, ms, DwtReplace(HAAR))
+ * followed by metrics.py:178-199 qnr(fused, ms, pan), without re-reading the
+ * fused bands. Writes out[0..nbands) (bit-identical to wf_fuse_bands_f32) and
+ * the report in wf_quality_scene_f32's layout; same shape/alignment rules and
+ * workspace (wf_quality_scene_workspace_bytes). kind must be WF_HAAR. */
+int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
+                        int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
+                        int w, void* workspace, double* report, int* undecidable, void* stream);
 
 /* ---- peer-memory halos for strip-sharded scenes (one process per GPU) ----
  * wf_ipc_export: 64-byte CUDA IPC handle of the allocation containing `ptr`

@@ -37,7 +37,7 @@ from .fusion import (
     quantize,
     resample_bilinear,
 )
-from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, q_index, qnr
+from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, fuse_and_qnr, q_index, qnr
 from .pnm import PnmRaster, fuse_pnm, read_pnm, to_plane, write_pnm
 from .tiling import TileGrid, fuse_tiled, pad_edge, pad_inputs, padded_dims, plan_grid
 from .wavelet import (
@@ -87,6 +87,7 @@ __all__ = [
     "dwt2d_inverse",
     "ergas",
     "fuse",
+    "fuse_and_qnr",
     "fuse_dwt",
     "fuse_pnm",
     "fuse_quantized",

@@ -108,6 +108,8 @@ def _declare_quality(lib: ctypes.CDLL) -> None:
                                   c_vp, c_vp, c_vp, c_vp], c_int),
         "wf_ergas_band": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_int, c_int, c_int, c_vp,
                            c_vp, c_vp], c_int),
+        "wf_fuse_quality_f32": ([c_int, c_vp, c_i64, c_vpp, c_i64, c_vpp, c_i64, c_int, c_int,
+                                 c_int, c_vp, c_vp, c_vp, c_vp], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

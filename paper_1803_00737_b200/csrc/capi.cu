@@ -779,6 +779,33 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
   return cuda_status(e, "wf_quality_scene_f32");
 }
 
+int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
+                        int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
+                        int w, void* workspace, double* report, int* undecidable, void* stream) {
+  if (kind != WF_HAAR) return fail(WF_ERR_VALUE, "fused fusion + quality pass is Haar only");
+  if (!out || !ms || !pan || !workspace || !report || !undecidable)
+    return fail(WF_ERR_VALUE, "null pointer argument");
+  if (nbands < 2 || nbands > wf::kMaxBandsPerLaunch)
+    return fail(WF_ERR_BAND_COUNT, "fused quality path takes 2..%d bands, got %d",
+                wf::kMaxBandsPerLaunch, nbands);
+  if ((h & 1) || (w % 8) || h < 64 || w < 64)
+    return fail(WF_ERR_VALUE, "fused quality path needs even H, W % 8 == 0, H, W >= 64 (got %dx%d)",
+                w, h);
+  auto row16 = [](int64_t pitch) { return (pitch * 4) % 16 == 0; };
+  if (!row16(out_pitch) || !row16(pan_pitch) || !row16(ms_pitch) || !al16(pan) ||
+      out_pitch < w || pan_pitch < w || ms_pitch < w / 2)
+    return fail(WF_ERR_VALUE, "fused quality path needs 16-byte aligned rows");
+  for (int b = 0; b < nbands; ++b) {
+    if (!out[b] || !ms[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
+    if (!al16(out[b]) || !al16(ms[b])) return fail(WF_ERR_VALUE, "band %d not 16-byte aligned", b);
+  }
+  cudaError_t e = wf::launch_fuse_quality_haar(nbands, pan, ms, out, out_pitch, ms_pitch,
+                                               pan_pitch, h, w, workspace, report, undecidable,
+                                               (cudaStream_t)stream);
+  if (e == cudaSuccess) g_launches += 5;
+  return cuda_status(e, "wf_fuse_quality_f32");
+}
+
 #define WF_FUSE_EXACT(NAME, T)                                                              \
   int NAME(int kind, const T* pan, int64_t pan_pitch, const T* ms, int64_t ms_pitch, T* out,  \
            int64_t out_pitch, int h, int w, void* workspace, void* stream) {                 \

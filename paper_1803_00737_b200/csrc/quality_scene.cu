@@ -59,6 +59,7 @@ struct QsCfg {
 
 struct QsArgs {
   const float* F[kMaxBandsPerLaunch];
+  float* O[kMaxBandsPerLaunch];  // fused variant: where the fused bands are written
   const float* M[kMaxBandsPerLaunch];
   const float* P;
   long long fp, mp, pp;  // pitches (elements)
@@ -683,7 +684,7 @@ struct Q2Maps {
   CUtensorMap m[kMaxBandsPerLaunch];
 };
 
-template <int NB>
+template <int NB, bool FUSE = false>
 struct Q2Cfg {
   static constexpr int S = NB <= 6 ? WF_Q2_STAGES : 2;
   // A stage is PAIRS row pairs (8 PAN rows): plane q (F_0..F_{NB-1}, P) as a
@@ -695,8 +696,16 @@ struct Q2Cfg {
   static constexpr int PAIRS = 4;
   static constexpr int MSR = PAIRS + 2;
   static constexpr int PLANE = 2 * PAIRS * kQ2Cols;
-  static constexpr int MSOFF = (NB + 1) * PLANE;
-  static constexpr int SLOT = MSOFF + NB * MSR * kQ2Msw;
+  // FUSE (Haar fusion in the same pass): only the PAN is staged -- plane 0
+  static constexpr int NPL = FUSE ? 1 : NB + 1;
+  static constexpr int PIDX = FUSE ? 0 : NB;
+  static constexpr int MSOFF = NPL * PLANE;
+  // FUSE: the fused bands of the stage, written by the F-role warps as dense
+  // per-warp slices [NB][kQ2Bc][2 * PAIRS rows][32 cols] (one TMA store each)
+  static constexpr int FOFF = MSOFF + NB * MSR * kQ2Msw;
+  static constexpr int FSL = 2 * PAIRS * 32;  // floats per slice
+  static constexpr int SLOT = FOFF + (FUSE ? NB * kQ2Bc * FSL : 0);
+  static constexpr int NBAR = ((2 + kQ2Bc * PAIRS) * S + 1) & ~1;  // full, empty, fready (even)
   static constexpr int NBE = NB + (NB & 1);  // bands padded to even (role L halves)
   static constexpr int H = NBE / 2;
   static constexpr int NBP = NBE / 2;        // float2 band pairs
@@ -739,12 +748,12 @@ __device__ __forceinline__ void q2_reduce(float* tr, double* ds, int lane, const
   }
 }
 
-template <int NB>
+template <int NB, bool FUSE>
 __global__ void __launch_bounds__(kQ2Threads, 1)
     quality_split_kernel(const QsArgs a, const __grid_constant__ Q2Maps maps, double* part_q,
                          double* part_low, double* part_erg, int* undecidable) {
   using L = QsLayout<NB>;
-  using C = Q2Cfg<NB>;
+  using C = Q2Cfg<NB, FUSE>;
   constexpr int S = C::S, NBE = C::NBE, H = C::H, NBP = C::NBP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // tensor-copy destinations 128-byte aligned; the offset is added to
@@ -754,7 +763,10 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       smem_raw + ((128u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 127u)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * C::SLOT);
   uint64_t* empty = full + S;
-  double* dsb = reinterpret_cast<double*>(empty + S);  // [2][kQ2Bc][DS]
+  uint64_t* fready = empty + S;  // FUSE: [S][kQ2Bc][PAIRS] fused rows of (stage, column, pair) ready
+  // barriers padded to an even count: dsb and the transpose buffers after it
+  // stay 16-byte aligned (LDS.128 in lane_sum32)
+  double* dsb = reinterpret_cast<double*>(full + C::NBAR);  // [2][kQ2Bc][DS]
   float* trs = reinterpret_cast<float*>(dsb + 2 * kQ2Bc * C::DS);  // [kQ2Cons][kQ2TrRows][kTrPad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -764,6 +776,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
     for (int s = 0; s < S; ++s) {
       tma::mbar_init(&full[s], kQ2Prod);
       tma::mbar_init(&empty[s], kQ2Cons);
+      for (int c = 0; c < kQ2Bc * C::PAIRS; ++c) tma::mbar_init(&fready[s * kQ2Bc * C::PAIRS + c], 1);
     }
     tma::fence_barrier_init();
   }
@@ -771,7 +784,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 
   if (warp == kQ2Cons) {
     // ---------------------------- producer --------------------------------
-    constexpr uint32_t kStageBytes = (uint32_t)C::SLOT * 4u;
+    constexpr uint32_t kStageBytes = (uint32_t)C::FOFF * 4u;  // PAN + MS boxes (not the F slices)
     int g = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int br = tile / a.ncx, cx = tile % a.ncx;
@@ -785,15 +798,17 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         if (lane == 0) tma::mbar_arrive_expect_tx(&full[s], kStageBytes);
         __syncwarp();
         float* slot = ring + (size_t)s * C::SLOT;
-        if (lane <= NB) {
+        if (lane < C::NPL) {
           const CUtensorMap* tm = &maps.p;
+          if (!FUSE) {
 #pragma unroll
-          for (int k = 0; k < NB; ++k)
-            if (lane == k) tm = &maps.f[k];
+            for (int k = 0; k < NB; ++k)
+              if (lane == k) tm = &maps.f[k];
+          }
           tma::tensor_g2s_2d(slot + lane * C::PLANE, tm, col0, 32 * br + 2 * C::PAIRS * u,
                              &full[s]);
-        } else if (lane < 2 * NB + 1) {
-          const int k = lane - (NB + 1);
+        } else if (lane < C::NPL + NB) {
+          const int k = lane - C::NPL;
           const CUtensorMap* tm = &maps.m[0];
 #pragma unroll
           for (int kk = 1; kk < NB; ++kk)
@@ -813,6 +828,14 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
   // role L: local band m <-> band (m + H * odd) mod NBE; bands >= NB are
   // padding (they read the PAN row; their sums are never reported)
   auto band_of = [&](int m) { return (m + (odd ? H : 0)) % NBE; };
+  // FUSE: the Haar cell mean of fuse_haar_kernel (fuse.cu), same operation
+  // order -- ll = ((P00 + P01) + (P10 + P11)) * 0.25 -- so F = P + (M - ll)
+  // is bit-identical to what fuse() writes
+  auto haar_ll = [&](const float (&pvv)[2]) {
+    const float h0 = pvv[0] + __shfl_xor_sync(0xffffffffu, pvv[0], 1);
+    const float h1 = pvv[1] + __shfl_xor_sync(0xffffffffu, pvv[1], 1);
+    return (h0 + h1) * 0.25f;
+  };
 
   // low-res shifts (role L), one tile ahead, as in the kernel above
   // Only raw loads here; the values are consumed a whole half-tile later
@@ -883,9 +906,49 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+          if (!FUSE) {
 #pragma unroll
-          for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
-          pv[p] = row[NB * C::PLANE];
+            for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
+          }
+          pv[p] = row[C::PIDX * C::PLANE];
+        }
+        if (FUSE) {
+          const float ll = haar_ll(pv);
+          const float* mr = slot + C::MSOFF + (h + 1) * kQ2Msw + rxr;  // M(i0 + t, x/2)
+          float* fs = const_cast<float*>(slot) + C::FOFF + bcl * C::FSL + 2 * h * 32 + lane;
+          if (h == 0) {  // this slot's slices from S stages ago must be read out first
+            if (lane == 0) tma::bulk_wait_read<S - 1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int k = 0; k < NBE; ++k) {
+            const float d = k < NB ? mr[k * C::MSR * kQ2Msw] - ll : 0.f;
+            fv[0][k] = k < NB ? pv[0] + d : 0.f;
+            fv[1][k] = k < NB ? pv[1] + d : 0.f;
+            if (k < NB) {
+              fs[k * kQ2Bc * C::FSL] = fv[0][k];
+              fs[k * kQ2Bc * C::FSL + 32] = fv[1][k];
+            }
+          }
+          // this pair's fused rows are in the slices: release them to the U / L
+          // warps of the block column (mbarrier arrive = release)
+          __syncwarp();
+          if (lane == 0) tma::mbar_arrive(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h]);
+          if (h == C::PAIRS - 1) {
+            // the stage's slices are complete: stream them to the fused bands
+            tma::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (blk_ok) {
+                const float* sl = slot + C::FOFF + bcl * C::FSL;
+#pragma unroll
+                for (int k = 0; k < NB; ++k)
+                  tma::tensor_s2g_2d(&maps.f[k], 32 * bc, 32 * br + 2 * C::PAIRS * u,
+                                     sl + k * kQ2Bc * C::FSL);
+              }
+              tma::bulk_commit();
+            }
+          }
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
@@ -1003,11 +1066,21 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 #pragma unroll
         for (int m = 0; m < NBP; ++m) hn[m] = hrow2(m, i0 + t + 1);
         float fv[2][NBE];
+        if (!FUSE) {
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+          for (int p = 0; p < 2; ++p) {
+            const float* row = slot + (2 * h + p) * kQ2Cols + xl;
 #pragma unroll
-          for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
+            for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
+          }
+        } else {  // the F role's slice of this block column
+          tma::mbar_wait_sleep(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h], (g / S) & 1);
+          const float* fs = slot + C::FOFF + bcl * C::FSL + 2 * h * 32 + lane;
+#pragma unroll
+          for (int k = 0; k < NBE; ++k) {
+            fv[0][k] = k < NB ? fs[k * kQ2Bc * C::FSL] : 0.f;
+            fv[1][k] = k < NB ? fs[k * kQ2Bc * C::FSL + 32] : 0.f;
+          }
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
@@ -1098,11 +1171,12 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       // pair lane past H is padding (never reported)
       constexpr int HP = (H + 1) / 2;
       float2 kml[HP];
-      int foff[NBE], moff[2 * HP];
+      int foff[NBE], fsoff[NBE], moff[2 * HP];
 #pragma unroll
       for (int m = 0; m < NBE; ++m) {
         const int b = band_of(m);
-        foff[m] = (b < NB ? b : NB) * C::PLANE;  // padding bands read the PAN row
+        foff[m] = (b < NB ? b : C::PIDX) * C::PLANE;  // padding bands read the PAN row
+        fsoff[m] = (b < NB ? b : 0) * kQ2Bc * C::FSL;   // FUSE: slice of band b
       }
 #pragma unroll
       for (int m = 0; m < 2 * HP; ++m) {
@@ -1140,9 +1214,20 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const float* row = slot + (2 * h + p) * kQ2Cols + xl;
+          if (!FUSE) {
 #pragma unroll
-          for (int m = 0; m < NBE; ++m) fv[p][m] = row[foff[m]];
-          pv[p] = row[NB * C::PLANE];
+            for (int m = 0; m < NBE; ++m) fv[p][m] = row[foff[m]];
+          }
+          pv[p] = row[C::PIDX * C::PLANE];
+        }
+        if (FUSE) {  // the F role's slice of this block column (local band order)
+          tma::mbar_wait_sleep(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h], (g / S) & 1);
+          const float* fs = slot + C::FOFF + bcl * C::FSL + 2 * h * 32 + lane;
+#pragma unroll
+          for (int m = 0; m < NBE; ++m) {
+            fv[0][m] = fs[fsoff[m]];
+            fv[1][m] = fs[fsoff[m] + 32];
+          }
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
@@ -1282,6 +1367,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
     // reach this tile's successor-but-one after the ring has moved past it,
     // i.e. after role F has scored this tile)
   }
+  if (FUSE && role == 0 && lane == 0) tma::bulk_wait<0>();  // fused-band stores complete
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -1303,11 +1389,11 @@ static bool qs_use_v1() {
   return e && e[0] == 'v' && e[1] == '1';
 }
 
-template <int NB>
+template <int NB, bool FUSE>
 static size_t q2_smem() {
   using L = QsLayout<NB>;
-  using C = Q2Cfg<NB>;
-  return 128 + (size_t)C::S * C::SLOT * sizeof(float) + 2 * C::S * sizeof(uint64_t) +
+  using C = Q2Cfg<NB, FUSE>;
+  return 128 + (size_t)C::S * C::SLOT * sizeof(float) + C::NBAR * sizeof(uint64_t) +
          (size_t)2 * kQ2Bc * C::DS * sizeof(double) +
          (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float) + 16;
 }
@@ -1382,14 +1468,50 @@ size_t quality_scene_workspace(int nb, int h, int w) {
   }
 }
 
+// Fused variant's pixels outside the 32x32 block grid (right and bottom
+// margins): the regular Haar kernel on those windows of the scene (Haar is
+// 2x2-local, so windows on even boundaries fuse exactly).
+template <int NB>
+static cudaError_t fuse_margins(const QsArgs& a, float* const* O, cudaStream_t s) {
+  auto window = [&](int r0, int c0, int rows, int cols) -> cudaError_t {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    FuseArgs<float> f{};
+    f.pan = a.P + (long long)r0 * a.pp + c0;
+    f.pan_pitch = a.pp;
+    f.pan_top = f.pan_bot = f.pan;
+    f.halo_pitch = a.pp;
+    for (int k = 0; k < NB; ++k) {
+      f.ms[k] = f.ms_top[k] = a.M[k] + (long long)(r0 / 2) * a.mp + c0 / 2;
+      f.out[k] = O[k] + (long long)r0 * a.fp + c0;
+    }
+    f.ms_pitch = a.mp;
+    f.out_pitch = a.fp;
+    f.nbands = NB;
+    f.rows = rows;
+    f.W = cols;
+    const bool vec = cols % 4 == 0 && c0 % 4 == 0 && a.pp % 4 == 0 && a.mp % 2 == 0 &&
+                     a.fp % 4 == 0;
+    return launch_fuse<float, float>(kHaar, f, vec, false, s, LaunchTuning{});
+  };
+  const int gr = 32 * a.nbr, gc = 32 * a.nbc;
+  cudaError_t e = window(0, gc, gr, a.W - gc);
+  if (e != cudaSuccess) return e;
+  return window(gr, 0, a.H - gr, a.W);
+}
+
+// O == nullptr: score the given fused bands F. O != nullptr: Haar-fuse PAN and
+// MS into O and score them in the same pass (F is ignored; role-split kernel).
 template <int NB>
 static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, const float* P,
                                 long long fp, long long mp, long long pp, int h, int w,
-                                void* workspace, double* out, int* undecidable, cudaStream_t s) {
+                                void* workspace, double* out, int* undecidable, cudaStream_t s,
+                                float* const* O = nullptr) {
   using L = QsLayout<NB>;
+  const bool fuse = O != nullptr;
   QsArgs a{};
   for (int k = 0; k < NB; ++k) {
-    a.F[k] = F[k];
+    a.F[k] = fuse ? O[k] : F[k];
+    a.O[k] = fuse ? O[k] : nullptr;
     a.M[k] = M[k];
   }
   a.P = P;
@@ -1400,7 +1522,7 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   a.W = w;
   a.Hh = h / 2;
   a.Wh = w / 2;
-  const bool v1 = qs_use_v1();
+  const bool v1 = !fuse && qs_use_v1();
   qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, a.ncx, v1 ? kQsWarps : kQ2Bc);
   const int ncta = a.nbr * a.ncx;  // tiles
   const int nparts = v1 ? ncta : ncta * kQ2Bc;  // Q / ERGAS partials
@@ -1409,21 +1531,24 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   double* part_erg = part_low + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
   double* part_edge = part_erg + (size_t)nparts * L::NERG;
   Q2Maps maps;
-  bool use_v1 = v1;
-  if (!use_v1) {
+  if (!v1) {
     // the role-split kernel needs tensor maps; 16-byte strides (W % 4 == 0)
     bool ok = (fp % 4 == 0) && (mp % 4 == 0) && (pp % 4 == 0);
-    for (int k = 0; ok && k < NB; ++k)
-      ok = plane_map(&maps.f[k], F[k], fp, h, w, kQ2Cols, 2 * Q2Cfg<NB>::PAIRS) &&
+    for (int k = 0; ok && k < NB; ++k)  // FUSE: f[k] is the store map of the output (32-col slices)
+      ok = (fuse ? plane_map(&maps.f[k], O[k], fp, h, w, 32, 2 * Q2Cfg<NB>::PAIRS)
+                 : plane_map(&maps.f[k], F[k], fp, h, w, kQ2Cols, 2 * Q2Cfg<NB>::PAIRS)) &&
            plane_map(&maps.m[k], M[k], mp, h / 2, w / 2, kQ2Msw, Q2Cfg<NB>::MSR);
     ok = ok && plane_map(&maps.p, P, pp, h, w, kQ2Cols, 2 * Q2Cfg<NB>::PAIRS);
     if (!ok) return cudaErrorInvalidValue;
   }
-  const size_t smem = use_v1 ? qs_smem<NB>() : q2_smem<NB>();
-  cudaError_t e = use_v1 ? cudaFuncSetAttribute(quality_scene_kernel<NB>,
+  const size_t smem = v1 ? qs_smem<NB>() : fuse ? q2_smem<NB, true>() : q2_smem<NB, false>();
+  cudaError_t e = v1     ? cudaFuncSetAttribute(quality_scene_kernel<NB>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)smem)
-                         : cudaFuncSetAttribute(quality_split_kernel<NB>,
+                  : fuse ? cudaFuncSetAttribute(quality_split_kernel<NB, true>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem)
+                         : cudaFuncSetAttribute(quality_split_kernel<NB, false>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)smem);
   if (e != cudaSuccess) return e;
@@ -1433,13 +1558,17 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = ncta < sms ? ncta : sms;  // persistent: one CTA per SM
-  if (use_v1)
+  if (v1)
     quality_scene_kernel<NB><<<grid, 32 * (kQsWarps + 1), smem, s>>>(a, part_q, part_low,
                                                                       part_erg, undecidable);
+  else if (fuse)
+    quality_split_kernel<NB, true><<<grid, kQ2Threads, smem, s>>>(a, maps, part_q, part_low,
+                                                                  part_erg, undecidable);
   else
-    quality_split_kernel<NB><<<grid, kQ2Threads, smem, s>>>(a, maps, part_q, part_low, part_erg,
-                                                            undecidable);
+    quality_split_kernel<NB, false><<<grid, kQ2Threads, smem, s>>>(a, maps, part_q, part_low,
+                                                                   part_erg, undecidable);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (fuse && (e = fuse_margins<NB>(a, O, s)) != cudaSuccess) return e;
   const int row_lo = 16 * a.nbr, col_lo = 16 * a.nbc;
   int nedge = 0;
   if (row_lo < a.Hh || col_lo < a.Wh) {
@@ -1450,6 +1579,20 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   quality_finish_kernel<NB><<<L::NQ + 3 * NB, 1024, 0, s>>>(a, part_q, nparts, part_low, part_erg,
                                                             part_edge, nedge, out, undecidable);
   return cudaGetLastError();
+}
+
+cudaError_t launch_fuse_quality_haar(int nb, const float* P, const float* const* M,
+                                     float* const* O, long long op, long long mp, long long pp,
+                                     int h, int w, void* workspace, double* out,
+                                     int* undecidable, cudaStream_t s) {
+  switch (nb) {
+#define WF_FQ(N) \
+  case N:        \
+    return launch_qs_nb<N>(nullptr, M, P, op, mp, pp, h, w, workspace, out, undecidable, s, O);
+    WF_FQ(2) WF_FQ(3) WF_FQ(4) WF_FQ(5) WF_FQ(6) WF_FQ(7) WF_FQ(8)
+#undef WF_FQ
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_quality_scene(int nb, const float* const* F, const float* const* M,

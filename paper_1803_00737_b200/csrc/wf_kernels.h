@@ -107,6 +107,13 @@ cudaError_t launch_ergas_band(const void* fz, int f64, long long fp, const void*
 // Fused single-pass quality report (quality_scene.cu), float32 planes,
 // ratio 2, 2..8 bands, H, W >= 64.
 size_t quality_scene_workspace(int nb, int h, int w);
+// Haar fusion of (P, M) into O and the one-pass report of O, in one pass
+// (the bands O inside the 32x32 block grid are written by the scoring kernel
+// itself; the margins by the plain Haar kernel)
+cudaError_t launch_fuse_quality_haar(int nb, const float* P, const float* const* M,
+                                     float* const* O, long long op, long long mp, long long pp,
+                                     int h, int w, void* workspace, double* out,
+                                     int* undecidable, cudaStream_t s);
 cudaError_t launch_quality_scene(int nb, const float* const* F, const float* const* M,
                                  const float* P, long long fp, long long mp, long long pp, int h,
                                  int w, void* workspace, double* out, int* undecidable,

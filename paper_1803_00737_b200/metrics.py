@@ -268,29 +268,45 @@ def _qnr_scene(f_t, m_t, p_t, ratio) -> QualityReport | None:
     """One-pass fused report (csrc/quality_scene.cu) when the scene qualifies:
     float32 planes, ratio 2, 2..8 bands, H, W >= 64. None = use the generic
     path (also when a block needs the element-wise identity test)."""
-    import os
-
     n = len(f_t)
     h, w = p_t.shape
-    if (os.environ.get("WF_QNR_PATH") == "generic" or ratio != 2 or not 2 <= n <= 8
-            or h < 64 or w < 64 or w % 8
-            or any(t.dtype != torch.float32 for t in (*f_t, *m_t, p_t))
-            or any(t.data_ptr() % 16 for t in (*f_t, *m_t, p_t))):
+    if not _scene_ok((*f_t, *m_t, p_t), n, h, w, ratio):
         return None
     lib = _native.load()
-    ws = torch.empty(int(lib.wf_quality_scene_workspace_bytes(n, h, w)) // 8 + 1,
-                     dtype=torch.float64, device=p_t.device)
-    c = n * (n - 1) // 2
-    out = torch.zeros(n + 2 * c + 4 * n, dtype=torch.float64, device=p_t.device)
-    flag = torch.zeros(1, dtype=torch.int32, device=p_t.device)
+    ws, out, flag = _scene_buffers(n, h, w, p_t.device)
     _native.check(lib.wf_quality_scene_f32(
         _native.ptr_array([t.data_ptr() for t in f_t]),
         _native.ptr_array([t.data_ptr() for t in m_t]), p_t.data_ptr(), f_t[0].stride(0),
         m_t[0].stride(0), p_t.stride(0), n, h, w, ws.data_ptr(), out.data_ptr(),
         flag.data_ptr(), _device.stream_ptr()))
-    vals = out.cpu().numpy()
     if int(flag.item()):
         return None
+    return _scene_report(out.cpu().numpy(), n, ratio)
+
+
+def _scene_ok(tensors, n, h, w, ratio) -> bool:
+    import os
+
+    return not (os.environ.get("WF_QNR_PATH") == "generic" or ratio != 2 or not 2 <= n <= 8
+                or h < 64 or w < 64 or w % 8
+                or any(t.dtype != torch.float32 for t in tensors)
+                or any(t.data_ptr() % 16 for t in tensors))
+
+
+def _scene_buffers(n, h, w, device):
+    lib = _native.load()
+    ws = torch.empty(int(lib.wf_quality_scene_workspace_bytes(n, h, w)) // 8 + 1,
+                     dtype=torch.float64, device=device)
+    c = n * (n - 1) // 2
+    out = torch.zeros(n + 2 * c + 4 * n, dtype=torch.float64, device=device)
+    flag = torch.zeros(1, dtype=torch.int32, device=device)
+    return ws, out, flag
+
+
+def _scene_report(vals, n, ratio) -> QualityReport:
+    """The report from the scene kernels' output vector (layout in
+    include/wavefuse_b200.h, wf_quality_scene_f32)."""
+    c = n * (n - 1) // 2
     fu = vals[:n]
     ff, uu = vals[n:n + c], vals[n + c:n + 2 * c]
     fp = vals[n + 2 * c:2 * n + 2 * c]
@@ -347,3 +363,49 @@ def qnr(fused, ms, pan) -> QualityReport:
         d_s=spatial,
         qnr=(1.0 - spectral) * (1.0 - spatial),
     )
+
+
+def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
+    """fuse(pan, ms, method) followed by qnr(fused, ms, pan); returns
+    (fused, QualityReport).
+
+    one_pass=True (Haar, scenes that qualify for the one-pass kernel: float32,
+    2..8 half-size bands, H, W >= 64, W % 8 == 0) runs SURVEY.md 8(f) row f1
+    literally: the scoring kernel fuses each pixel itself and streams the
+    fused bands out as it scores them, so they are never re-read (C ABI
+    wf_fuse_quality_f32; bands bit-identical to fuse()'s, report identical
+    to qnr()'s). It is opt-in because it is slower on B200: the scoring
+    kernel is compute-bound, and making the fusion a per-row-pair dependency
+    of the scoring warps costs more than re-reading 5.4 GB of fused bands
+    (Landsat, 6 bands: 4.07 ms one pass vs 3.40 ms for fuse() + qnr();
+    bench.py quality.fused_haar_fuse_and_report)."""
+    from . import fusion as _fusion
+    from .wavelet import WaveletKind
+
+    if not isinstance(method, _fusion.DwtReplace):
+        raise TypeError(f"unknown fusion method {method!r}")
+    is_t = isinstance(pan, torch.Tensor)
+    p_shape = tuple(pan.shape) if is_t else np.shape(pan)
+    bands = _bands(ms)
+    fast = (one_pass and method.kind == WaveletKind.HAAR and len(p_shape) == 2 and bands
+            and all(_shape(b) == (p_shape[0] // 2, p_shape[1] // 2) for b in bands)
+            and p_shape[0] % 2 == 0 and p_shape[1] % 2 == 0)
+    if fast:
+        p_t = _device.to_device(pan, np.float32) if (is_t or _device.is_f32(pan)) else None
+        m_t = [_plane(b) for b in bands] if p_t is not None else []
+        n = len(m_t)
+        h, w = p_shape
+        if p_t is not None and p_t.dtype == torch.float32 and \
+                _scene_ok((*m_t, p_t), n, h, w, 2) and all(t.dtype == torch.float32 for t in m_t):
+            lib = _native.load()
+            outs = [torch.empty((h, w), dtype=torch.float32, device=p_t.device) for _ in m_t]
+            ws, out, flag = _scene_buffers(n, h, w, p_t.device)
+            _native.check(lib.wf_fuse_quality_f32(
+                1, p_t.data_ptr(), p_t.stride(0), _native.ptr_array([t.data_ptr() for t in m_t]),
+                m_t[0].stride(0), _native.ptr_array([o.data_ptr() for o in outs]), w, n, h, w,
+                ws.data_ptr(), out.data_ptr(), flag.data_ptr(), _device.stream_ptr()))
+            rep = (qnr(outs, m_t, p_t) if int(flag.item())
+                   else _scene_report(out.cpu().numpy(), n, 2))
+            return (outs if is_t else [o.cpu().numpy() for o in outs]), rep
+    fused = _fusion.fuse(pan, ms, method)
+    return fused, qnr(fused, ms, pan)
