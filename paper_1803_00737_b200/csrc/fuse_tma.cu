@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
 #pragma unroll
           // E = 2*ms - LL: 2*ms is exact, so one rounding like (ms + ms) - LL
           for (int jj = 0; jj < 3; ++jj) e[jj] = fma(Acc(2), m3[jj], -ll[jj]);
-          if (valid) {
+          {  // computed by every lane; only the stores are predicated (no branch per band)
             T* orow = a.out[0];
 #pragma unroll
             for (int bb = 1; bb < NB; ++bb)
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
                     make_float2(pa[p][2], pa[p][3]),
                     __ffma2_rn(wc, make_float2(v1p, v1p), __fmul2_rn(wp, make_float2(v0p, v0p))));
                 const Acc o[4] = {o01.x, o01.y, o23.x, o23.y};
-                store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
               }
             } else {
 #pragma unroll
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
                 const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
                 const Acc o[4] = {pa[p][0] + fma(h0, v0, h2 * vm), pa[p][1] + fma(h1, v0, h3 * vm),
                                   pa[p][2] + fma(h0, v1, h2 * v0), pa[p][3] + fma(h1, v1, h3 * v0)};
-                store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
               }
             }
           }
