@@ -503,6 +503,7 @@ def run_ours(args, rank, world, local_rank):
                 "frac": round(achieved / peak, 4),
                 "traffic": ncu_traffic(f"fuse_{kind.value}_b6"),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "frac_of_8tbs_nameplate": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": nbytes,
                 "kernel": ("fuse_haar_kernel<f32,B=6>" if kind is WaveletKind.HAAR
                            else "fuse_d4_tma_kernel<f32,B=6,4 consumer warps>"),
@@ -555,6 +556,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": hr["roofline"],
             "e2e": hr["e2e"],
             "cpu_baseline": cpu.get("haar"),
+            # both rates -- band-MPix/s = B x scene-MPix/s
+            "band_mpix_per_s": round(B * hr["value"], 1),
             "daub4": {
                 "value": round(results["daub4"]["value"], 3),
                 "ms_per_step": round(results["daub4"]["ms_per_step"], 4),
