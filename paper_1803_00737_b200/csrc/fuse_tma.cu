@@ -28,6 +28,9 @@
 #include "wf_kernels.h"
 #include "wf_tma.cuh"
 
+#include <stdlib.h>
+#include <string.h>
+
 namespace wf {
 
 // MIN_CTAS: the 4-byte and 1-byte rings (~44 KB) fit 4-5 CTAs per SM, so
@@ -117,6 +120,73 @@ __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
   }
 }
 
+// The producer warp of the pipelined D4 kernels: for every row pair of the
+// task, bulk copies (UBLKCP) of the two new PAN rows -- each as a HALO-wide
+// left piece, the main span and a HALO-wide right piece, the periodic wrap
+// applied to the halo pieces' source columns -- and of one MS row per band
+// (left halo + span) into ring slot n % S, with the transaction bytes on the
+// slot's full barrier. Slot layout: [PAN row | PAN row | NB x MS row], rows of
+// CW + 2*HALO and CW/2 + HALO elements.
+template <typename T, int NB, int CW, int HALO>
+__device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slots, uint64_t* full,
+                                             uint64_t* empty, int base, int len, int i0,
+                                             int nloads, int lane) {
+  constexpr int PROW = CW + 2 * HALO;
+  constexpr int MROW = CW / 2 + HALO;
+  constexpr int SLOT = 2 * PROW + NB * MROW;
+  const int W = a.W, Wh = a.W >> 1;
+  const TmaRows<T> pan{a.pan, a.pan_top, a.pan_bot, a.pan_pitch, a.halo_pitch, a.rows};
+  const uint32_t pan_row_bytes = (uint32_t)((len + 2 * HALO) * sizeof(T));
+  const uint32_t ms_row_bytes = (uint32_t)((len / 2 + HALO) * sizeof(T));
+  // per-lane copy role (fixed for the whole task)
+  const int q = lane / 3, piece = lane % 3;  // lanes 0..5: PAN row q, piece
+  const int mb = (lane - 6) >> 1, mpiece = (lane - 6) & 1;  // lanes 6..: MS band, piece
+  const int lcol = wrap(base - HALO, W), rcol = (base + len) % W;
+  const int mlcol = wrap((base >> 1) - HALO, Wh);
+  for (int n = 0; n < nloads; ++n) {
+    const int s = n % S, r = n / S;
+    if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
+    __syncwarp();
+    const bool with_ms = n >= 1;
+    if (lane == 0)
+      tma::mbar_arrive_expect_tx(&full[s],
+                                 2 * pan_row_bytes + (with_ms ? NB * ms_row_bytes : 0u));
+    __syncwarp();
+    T* slot = slots + (size_t)s * SLOT;
+    const int k = n - 2;  // row pair index relative to i0
+    if (lane < 6) {
+      const T* row = pan.row(2 * (i0 + k) + 2 + q);
+      T* dst = slot + q * PROW;
+      if (piece == 0)
+        tma::bulk_g2s(dst, row + lcol, HALO * sizeof(T), &full[s]);
+      else if (piece == 1)
+        tma::bulk_g2s(dst + HALO, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
+      else
+        tma::bulk_g2s(dst + HALO + len, row + rcol, HALO * sizeof(T), &full[s]);
+    } else if (with_ms && lane < 6 + 2 * NB) {
+      const int mrow = i0 + k;
+      const T* mr = a.ms[0];
+#pragma unroll
+      for (int b = 1; b < NB; ++b)  // static indexing keeps the band table in the param bank
+        if (mb == b) mr = a.ms[b];
+      if (mrow < 0) {
+        mr = a.ms_top[0];
+#pragma unroll
+        for (int b = 1; b < NB; ++b)
+          if (mb == b) mr = a.ms_top[b];
+      } else {
+        mr += (long long)mrow * a.ms_pitch;
+      }
+      T* dst = slot + 2 * PROW + mb * MROW;
+      if (mpiece == 0)
+        tma::bulk_g2s(dst, mr + mlcol, HALO * sizeof(T), &full[s]);
+      else
+        tma::bulk_g2s(dst + HALO, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)),
+                      &full[s]);
+    }
+  }
+}
+
 template <typename T, int NB, int NCW>
 __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
     fuse_d4_tma_kernel(const FuseArgs<T> a, int S) {
@@ -152,57 +222,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
   __syncthreads();
 
   if (warp == NCW) {
-    // ------------------------------ producer ------------------------------
-    const TmaRows<T> pan{a.pan, a.pan_top, a.pan_bot, a.pan_pitch, a.halo_pitch, a.rows};
-    const uint32_t pan_row_bytes = (uint32_t)((len + 2 * HALO) * sizeof(T));
-    const uint32_t ms_row_bytes = (uint32_t)((len / 2 + HALO) * sizeof(T));
-    // per-lane copy role (fixed for the whole task)
-    const int q = lane / 3, piece = lane % 3;  // lanes 0..5: PAN row q, piece
-    const int mb = (lane - 6) >> 1, mpiece = (lane - 6) & 1;  // lanes 6..: MS band, piece
-    const int lcol = wrap(base - HALO, W), rcol = (base + len) % W;
-    const int mlcol = wrap((base >> 1) - HALO, Wh);
-    for (int n = 0; n < nloads; ++n) {
-      const int s = n % S, r = n / S;
-      if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
-      __syncwarp();
-      const bool with_ms = n >= 1;
-      if (lane == 0)
-        tma::mbar_arrive_expect_tx(&full[s],
-                                   2 * pan_row_bytes + (with_ms ? NB * ms_row_bytes : 0u));
-      __syncwarp();
-      T* slot = slots + (size_t)s * SLOT;
-      const int k = n - 2;  // row pair index relative to i0
-      if (lane < 6) {
-        const T* row = pan.row(2 * (i0 + k) + 2 + q);
-        T* dst = slot + q * PROW;
-        if (piece == 0)
-          tma::bulk_g2s(dst, row + lcol, HALO * sizeof(T), &full[s]);
-        else if (piece == 1)
-          tma::bulk_g2s(dst + HALO, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
-        else
-          tma::bulk_g2s(dst + HALO + len, row + rcol, HALO * sizeof(T), &full[s]);
-      } else if (with_ms && lane < 6 + 2 * NB) {
-        const int mrow = i0 + k;
-        const T* mr = a.ms[0];
-#pragma unroll
-        for (int b = 1; b < NB; ++b)  // static indexing keeps the band table in the param bank
-          if (mb == b) mr = a.ms[b];
-        if (mrow < 0) {
-          mr = a.ms_top[0];
-#pragma unroll
-          for (int b = 1; b < NB; ++b)
-            if (mb == b) mr = a.ms_top[b];
-        } else {
-          mr += (long long)mrow * a.ms_pitch;
-        }
-        T* dst = slot + 2 * PROW + mb * MROW;
-        if (mpiece == 0)
-          tma::bulk_g2s(dst, mr + mlcol, HALO * sizeof(T), &full[s]);
-        else
-          tma::bulk_g2s(dst + HALO, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)),
-                        &full[s]);
-      }
-    }
+    produce_rows<T, NB, CW, HALO>(a, S, slots, full, empty, base, len, i0, nloads, lane);
     return;
   }
 
@@ -331,6 +351,242 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 8 bpp D4, v2 (the default for uint8). The same pipeline (produce_rows) and
+// the same per-pixel expression trees as fuse_d4_tma_kernel<float>, so the
+// bytes are bit-identical to quantize() of the f32 kernel's output; the
+// layout is chosen for an issue-bound kernel (v1 spent ~40% of its issue
+// slots on addressing, predication branches and register copies):
+//  * a thread owns 8 columns (a warp 256), so the +-2-column halo, the row
+//    low-pass of the halo half-column and the loop overhead are shared by
+//    twice as many pixels; PAN bytes arrive as 4 + 8 + 4-byte LDS words;
+//  * every value is packed over the row pair: the row low-pass of rows
+//    (2i+2, 2i+3), the vertical synthesis V = (h0,h1) E(i) + (h2,h3) E(i-1)
+//    of output rows (2i, 2i+1), the horizontal synthesis and the quantize
+//    all issue as FFMA2/FMUL2/FADD2 with broadcast taps and no operand
+//    shuffles (each packed lane rounds exactly like the scalar op);
+//  * each output row's 8 bytes leave as one predicated st.global.cs.v2.
+// ---------------------------------------------------------------------------
+#ifndef WF_U8X8_MIN_CTAS
+#define WF_U8X8_MIN_CTAS 4
+#endif
+
+__device__ __forceinline__ float u8f(uint32_t w, int byte) {
+  return (float)((w >> (8 * byte)) & 0xffu);
+}
+
+__device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n"
+      " @q st.global.cs.v2.b32 [%0], {%1, %2};\n}" ::"l"(p),
+      "r"(x), "r"(y), "r"((uint32_t)pred)
+      : "memory");
+}
+
+template <int NB, int NCW>
+__global__ void __launch_bounds__(32 * (NCW + 1), WF_U8X8_MIN_CTAS)
+    fuse_d4_u8x8_kernel(const FuseArgs<uint8_t> a, int S) {
+  constexpr int HALO = 16;
+  constexpr int CW = 256 * NCW;
+  constexpr int PROW = CW + 2 * HALO;
+  constexpr int MROW = CW / 2 + HALO;
+  constexpr int SLOT = 2 * PROW + NB * MROW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint8_t* slots = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)S * SLOT + 15) & ~size_t(15)));
+  uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb = (int)(blockIdx.x % (unsigned)a.n_colbands);
+  const int rt = (int)(blockIdx.x / (unsigned)a.n_colbands);
+  const int base = cb * CW;
+  const int len = min(CW, a.W - base);
+  const int npairs = a.rows >> 1;
+  const int i0 = rt * a.pairs_per_task;
+  const int i1 = min(i0 + a.pairs_per_task, npairs);
+  const int nloads = (i1 - i0) + 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], NCW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    produce_rows<uint8_t, NB, CW, HALO>(a, S, slots, full, empty, base, len, i0, nloads, lane);
+    return;
+  }
+
+  const D4 tp = d4_taps();
+  const float h0 = (float)tp.h0, h1 = (float)tp.h1, h2 = (float)tp.h2, h3 = (float)tp.h3;
+  const float2 H0 = make_float2(h0, h0), H1 = make_float2(h1, h1);
+  const float2 H2 = make_float2(h2, h2), H3 = make_float2(h3, h3);
+  const float2 H01 = make_float2(h0, h1), H23 = make_float2(h2, h3);
+  const int t = warp * 32 + lane;
+  const int rel = 8 * t;
+  const bool valid = rel < len;
+  const int c = base + rel;
+
+  float2 rprev[5];  // row low-pass of the previous PAN row pair, half-cols j-1 .. j+3
+  float2 pa[8];     // PAN rows (2i, 2i+1) at columns c .. c+7
+  // E(i-1) at half-cols j-1 .. j+3 of every band, carried from one row pair
+  // to the next in thread-private shared memory (a float4 + a float per band,
+  // conflict-free), not in 5*NB registers: registers then fit 4 CTAs per SM
+  float4* ep4 = reinterpret_cast<float4*>(empty + S) + t;  // [NB][NCW*32]
+  float* ep1 = reinterpret_cast<float*>(reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + t;
+
+#pragma unroll 2
+  for (int n = 0; n < nloads; ++n) {
+    const int s = n % S;
+    tma::mbar_wait_sleep(&full[s], (n / S) & 1);
+    const uint8_t* slot = slots + (size_t)s * SLOT;
+    // PAN columns c-2 .. c+9 of the slot's two rows, packed (row 0, row 1)
+    float2 x[12];
+    {
+      uint32_t w[2][4];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint8_t* pr = slot + q * PROW + HALO + rel;
+        w[q][0] = *reinterpret_cast<const uint32_t*>(pr - 4);
+        const uint2 m = *reinterpret_cast<const uint2*>(pr);
+        w[q][1] = m.x;
+        w[q][2] = m.y;
+        w[q][3] = *reinterpret_cast<const uint32_t*>(pr + 8);
+      }
+#pragma unroll
+      for (int m = 0; m < 12; ++m)
+        x[m] = make_float2(u8f(w[0][(m + 2) >> 2], (m + 2) & 3),
+                           u8f(w[1][(m + 2) >> 2], (m + 2) & 3));
+    }
+    float2 rn[5];
+#pragma unroll
+    for (int J = 0; J < 5; ++J)
+      rn[J] = __ffma2_rn(H3, x[2 * J + 3],
+                         __ffma2_rn(H2, x[2 * J + 2],
+                                    __ffma2_rn(H1, x[2 * J + 1], __fmul2_rn(H0, x[2 * J]))));
+    if (n >= 1) {
+      float ll[5];
+#pragma unroll
+      for (int J = 0; J < 5; ++J)
+        ll[J] = fma(h3, rn[J].y, fma(h2, rn[J].x, fma(h1, rprev[J].y, h0 * rprev[J].x)));
+      const int i = i0 + n - 2;
+      const long long off0 = (long long)(2 * i) * a.out_pitch + c;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const uint8_t* mr = slot + 2 * PROW + b * MROW + HALO + (rel >> 1);
+        const uint32_t mw = *reinterpret_cast<const uint32_t*>(mr);
+        float e[5];
+        e[0] = fma(2.0f, (float)mr[-1], -ll[0]);
+#pragma unroll
+        for (int J = 1; J < 5; ++J) e[J] = fma(2.0f, u8f(mw, J - 1), -ll[J]);
+        if (n >= 2) {
+          float ep[5];
+          {
+            const float4 q = ep4[b * NCW * 32];
+            ep[0] = ep1[b * NCW * 32];
+            ep[1] = q.x;
+            ep[2] = q.y;
+            ep[3] = q.z;
+            ep[4] = q.w;
+          }
+          float2 V[5];
+#pragma unroll
+          for (int J = 0; J < 5; ++J)
+            V[J] = __ffma2_rn(H01, make_float2(e[J], e[J]),
+                              __fmul2_rn(H23, make_float2(ep[J], ep[J])));
+          float2 r[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int k = m >> 1;
+            const float2 o =
+                __fadd2_rn(pa[m], (m & 1) ? __ffma2_rn(H1, V[k + 1], __fmul2_rn(H3, V[k]))
+                                          : __ffma2_rn(H0, V[k + 1], __fmul2_rn(H2, V[k])));
+            // imageio.py:115-123 quantize as in quantize_lanes(), but with the
+            // magic 2^23 + 2^16: the low 16 bits of r are then floor(c) itself
+            // as a signed 16-bit lane (the 2^16 carries out), so the clamp
+            // needs no lane offset
+            r[m] = __fadd2_rd(__fadd2_rn(o, make_float2(0.5f, 0.5f)),
+                              make_float2(8454144.0f, 8454144.0f));
+          }
+          uint32_t wq[2][2];
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const uint32_t l01 = __byte_perm(
+                  __float_as_uint(p ? r[4 * g].y : r[4 * g].x),
+                  __float_as_uint(p ? r[4 * g + 1].y : r[4 * g + 1].x), 0x5410);
+              const uint32_t l23 = __byte_perm(
+                  __float_as_uint(p ? r[4 * g + 2].y : r[4 * g + 2].x),
+                  __float_as_uint(p ? r[4 * g + 3].y : r[4 * g + 3].x), 0x5410);
+              wq[p][g] = __byte_perm(__vimin_s16x2_relu(l01, 0x00FF00FFu),
+                                     __vimin_s16x2_relu(l23, 0x00FF00FFu), 0x6420);
+            }
+          uint8_t* orow = a.out[0];
+#pragma unroll
+          for (int bb = 1; bb < NB; ++bb)
+            if (b == bb) orow = a.out[bb];
+          st_cs_v2_if(orow + off0, wq[0][0], wq[0][1], valid);
+          st_cs_v2_if(orow + off0 + a.out_pitch, wq[1][0], wq[1][1], valid);
+        }
+        ep4[b * NCW * 32] = make_float4(e[1], e[2], e[3], e[4]);
+        ep1[b * NCW * 32] = e[0];
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) pa[m] = x[m + 2];
+#pragma unroll
+    for (int J = 0; J < 5; ++J) rprev[J] = rn[J];
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
+  }
+}
+
+template <int NB, int NCW>
+static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
+                                  const LaunchTuning& tune) {
+  FuseArgs<uint8_t> a = a0;
+  constexpr int CW = 256 * NCW;
+  constexpr int SLOT = 2 * (CW + 32) + NB * (CW / 2 + 16);
+  const int npairs = a.rows >> 1;
+  int S = tune.d4_stages > 0 ? tune.d4_stages : (int)((32 * 1024) / SLOT);
+  if (S < 2) S = 2;
+  if (S > 16) S = 16;
+  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer thread)
+  const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
+                      (size_t)NB * NCW * 32 * 20;
+  auto kern = fuse_d4_u8x8_kernel<NB, NCW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  a.n_colbands = (a.W + CW - 1) / CW;
+  int P = tune.d4_pairs > 0 ? tune.d4_pairs : 32;
+  if (P > npairs) P = npairs;
+  a.pairs_per_task = P;
+  const long long n_row = (npairs + P - 1) / P;
+  a.n_tasks = n_row * a.n_colbands;
+  kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_u8x8(const FuseArgs<uint8_t>& a, cudaStream_t s,
+                               const LaunchTuning& tune) {
+  switch (a.nbands) {
+    case 1: return launch_u8x8_nb<1, 4>(a, s, tune);
+    case 2: return launch_u8x8_nb<2, 4>(a, s, tune);
+    case 3: return launch_u8x8_nb<3, 4>(a, s, tune);
+    case 4: return launch_u8x8_nb<4, 4>(a, s, tune);
+    case 5: return launch_u8x8_nb<5, 4>(a, s, tune);
+    case 6: return launch_u8x8_nb<6, 4>(a, s, tune);
+    case 7: return launch_u8x8_nb<7, 4>(a, s, tune);
+    case 8: return launch_u8x8_nb<8, 4>(a, s, tune);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename T, int NB, int NCW>
 static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const LaunchTuning& tune) {
   FuseArgs<T> a = a0;
@@ -367,6 +623,10 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
 
 template <typename T>
 cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune) {
+  if constexpr (sizeof(T) == 1) {
+    const char* v = getenv("WF_D4_U8");  // "v1": the 4-column kernel below
+    if (!(v && strcmp(v, "v1") == 0)) return launch_u8x8(a, s, tune);
+  }
   switch (a.nbands) {
     case 1: return launch_tma_nb<T, 1, 4>(a, s, tune);
     case 2: return launch_tma_nb<T, 2, 4>(a, s, tune);

@@ -156,3 +156,28 @@ def test_unaligned_widths_fall_back():
         ref = O.fuse_quantized(pan, ms, kname)
         for o, r in zip(got, ref):
             assert _flips(o, r) <= 2
+
+
+@pytest.mark.parametrize("shape,nb", [((64, 1024), 1), ((96, 2080), 3), ((130, 16000), 6),
+                                      ((34, 3104), 8), ((4, 32), 2)])
+@pytest.mark.parametrize("variant", ["v2", "v1"])
+def test_u8_d4_equals_quantized_f32_kernel(shape, nb, variant, monkeypatch):
+    """The 8 bpp D4 kernels (v2: 8 columns per thread, row-pair packed; v1:
+    the 4-column kernel, WF_D4_U8=v1) run the f32 kernel's expression trees,
+    so their bytes equal quantize() of the f32 kernel's output on the same
+    (integer-valued) inputs, bit for bit -- including partial column bands
+    (W not a multiple of the CTA's 1024 columns), 1..8 bands and values far
+    outside [0, 255] before the clamp."""
+    if variant == "v1":
+        monkeypatch.setenv("WF_D4_U8", "v1")
+    rng = np.random.default_rng(11 + nb)
+    H, W = shape
+    pan = rng.integers(0, 256, (H, W), dtype=np.uint8)
+    ms = [rng.integers(0, 256, (H // 2, W // 2), dtype=np.uint8) for _ in range(nb)]
+    m = wf.DwtReplace(wf.WaveletKind.DAUB4)
+    got = wf.fuse_quantized(torch.from_numpy(pan).cuda(),
+                            [torch.from_numpy(x).cuda() for x in ms], m)
+    f32 = wf.fuse(torch.from_numpy(pan.astype(np.float32)).cuda(),
+                  [torch.from_numpy(x.astype(np.float32)).cuda() for x in ms], m)
+    for g, f in zip(got, f32):
+        assert np.array_equal(g.cpu().numpy(), wf.quantize(f.cpu().numpy()))

@@ -1,4 +1,5 @@
-"""Time the 8 bpp kernels on the Landsat scene for several D4 row-run lengths."""
+"""Time the 8 bpp kernels on the Landsat scene: Haar, and D4 per kernel variant
+(WF_D4_U8), row-run length (WF_D4_PAIRS) and ring depth (WF_D4_STAGES)."""
 import os
 import sys
 
@@ -18,9 +19,18 @@ lib = _native.load()
 mp = _native.ptr_array([m.data_ptr() for m in ms])
 op = _native.ptr_array([o.data_ptr() for o in out])
 nbytes = H * W + B * (H * W // 4 + H * W)
-for kind, pairs in ((1, [0]), (2, [4, 8, 16, 32, 64])):
-    for p in pairs:
-        os.environ["WF_D4_PAIRS"] = str(p)
+# argv: configs "variant:pairs:stages" (0 = launcher default); D4 only when given
+configs = sys.argv[1:] or ["haar", "v2:32:0", "v2:16:0", "v2:64:0", "v1:32:0"]
+for cfg in configs:
+    if cfg == "haar":
+        kind, variant, p, st = 1, "v2", 0, 0
+    else:
+        variant, p, st = cfg.split(":")
+        kind, p, st = 2, int(p), int(st)
+    os.environ["WF_D4_U8"] = variant
+    os.environ["WF_D4_PAIRS"] = str(p)
+    os.environ["WF_D4_STAGES"] = str(st)
+    if True:
         run = lambda: _native.check(lib.wf_fuse_bands_u8(kind, pan.data_ptr(), W, mp, W // 2, op,
                                                          W, B, H, W, None))
         for _ in range(3):
@@ -33,5 +43,5 @@ for kind, pairs in ((1, [0]), (2, [4, 8, 16, 32, 64])):
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 20
-        print(f"u8 kind={kind} pairs={p}: {t:.3f} ms {nbytes / t / 1e6:.0f} GB/s "
+        print(f"u8 {cfg}: {t:.3f} ms {nbytes / t / 1e6:.0f} GB/s "
               f"{H * W / t / 1e3:.0f} MPix/s", flush=True)
