@@ -218,6 +218,28 @@ def run_reference(args, rank: int):
     print(json.dumps(line), flush=True)
 
 
+def init_dist(world, local_rank):
+    """One process per GPU: rank -> cuda:LOCAL_RANK, NCCL for the timing
+    max-reduction and barriers. WF_BENCH_BACKEND=gloo (plumbing checks on a
+    box with fewer GPUs than ranks: ranks share devices round-robin; they
+    never wait on one another inside a kernel) -- never for a reported
+    number."""
+    import torch
+
+    backend = os.environ.get("WF_BENCH_BACKEND", "nccl")
+    dev = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
+    torch.cuda.set_device(dev)
+    if world <= 1:
+        return None, dev
+    import torch.distributed as td
+
+    if backend == "nccl":
+        td.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        td.init_process_group(backend)
+    return td, dev
+
+
 # ---------------------------------------------------------------------------
 def measure_device(scene, kind, steps, warmup, dist, world, dev_index):
     """Device-resident throughput of the fused kernel (CUDA events on the
@@ -457,10 +479,10 @@ def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_launch": nbytes,
                          "traffic": ncu_traffic("fuse_haar_u8_kernel_6" if kind is WaveletKind.HAAR
-                                                else "fuse_d4_tma_kernel_unsigned_char__6__4"),
+                                                else "fuse_d4_u8x8_kernel_6"),
                          "kernel": ("fuse_haar_u8_kernel<B=6> (16-bit lanes)"
                                     if kind is WaveletKind.HAAR
-                                    else "fuse_d4_tma_kernel<u8,B=6,4 consumer warps>")},
+                                    else "fuse_d4_u8x8_kernel<B=6> (8 cols/thread, row-pair packed)")},
             "e2e": {"value": round(world * h * w * e2e_steps / sec / 1e6, 3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "wf_fuse_host_u8 (C ABI, pinned host buffers, strips of 1024 rows)",
@@ -475,13 +497,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_1803_00737_b200 import WaveletKind
     from paper_1803_00737_b200.scene import DeviceScene, scene_bytes
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as td
-
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        dist = td
+    dist, local_rank = init_dist(world, local_rank)
     scene = DeviceScene.synthetic(H, W, B, scene=rank)
     torch.cuda.synchronize()
     peak, peak_kind = peaks()
@@ -594,13 +610,7 @@ def run_strips(args, rank, world, local_rank):
 
     from paper_1803_00737_b200 import WaveletKind, _native, strips, synth
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as td
-
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        dist = td
+    dist, local_rank = init_dist(world, local_rank)
     n = args.strip_size
     r0, r1 = strips.strip_bounds(n, world, rank)
     rows = r1 - r0
@@ -697,13 +707,7 @@ def run_batch(args, rank, world, local_rank):
     from paper_1803_00737_b200 import _native, strips, synth
     from paper_1803_00737_b200.scene import DeviceScene
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as td
-
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        dist = td
+    dist, local_rank = init_dist(world, local_rank)
     mine = strips.shard(list(range(args.scenes)), rank, world)
     scenes = []
     out = None

@@ -371,8 +371,15 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
 #define WF_U8X8_MIN_CTAS 4
 #endif
 
+// byte `byte` of w as a float. ALU = false: I2F.U8 with a byte select (XU
+// pipe, quarter rate); ALU = true: PRMT zero-extend + I2FP.F32.U32 (ALU pipe),
+// two issue slots but off the conversion unit. Both are exact.
+template <bool ALU>
 __device__ __forceinline__ float u8f(uint32_t w, int byte) {
-  return (float)((w >> (8 * byte)) & 0xffu);
+  if constexpr (ALU)
+    return __uint2float_rn(__byte_perm(w, 0u, 0x4440u + (uint32_t)byte));
+  else
+    return (float)((w >> (8 * byte)) & 0xffu);
 }
 
 __device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, bool pred) {
@@ -383,8 +390,8 @@ __device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, boo
       : "memory");
 }
 
-template <int NB, int NCW>
-__global__ void __launch_bounds__(32 * (NCW + 1), WF_U8X8_MIN_CTAS)
+template <int NB, int NCW, int MINB, int CVT>
+__global__ void __launch_bounds__(32 * (NCW + 1), MINB)
     fuse_d4_u8x8_kernel(const FuseArgs<uint8_t> a, int S) {
   constexpr int HALO = 16;
   constexpr int CW = 256 * NCW;
@@ -458,8 +465,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), WF_U8X8_MIN_CTAS)
       }
 #pragma unroll
       for (int m = 0; m < 12; ++m)
-        x[m] = make_float2(u8f(w[0][(m + 2) >> 2], (m + 2) & 3),
-                           u8f(w[1][(m + 2) >> 2], (m + 2) & 3));
+        x[m] = make_float2(u8f<(CVT & 1) != 0>(w[0][(m + 2) >> 2], (m + 2) & 3),
+                           u8f<(CVT & 1) != 0>(w[1][(m + 2) >> 2], (m + 2) & 3));
     }
     float2 rn[5];
 #pragma unroll
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), WF_U8X8_MIN_CTAS)
         float e[5];
         e[0] = fma(2.0f, (float)mr[-1], -ll[0]);
 #pragma unroll
-        for (int J = 1; J < 5; ++J) e[J] = fma(2.0f, u8f(mw, J - 1), -ll[J]);
+        for (int J = 1; J < 5; ++J) e[J] = fma(2.0f, u8f<(CVT & 2) != 0>(mw, J - 1), -ll[J]);
         if (n >= 2) {
           float ep[5];
           {
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), WF_U8X8_MIN_CTAS)
   }
 }
 
-template <int NB, int NCW>
+template <int NB, int NCW, int MINB, int CVT>
 static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
                                   const LaunchTuning& tune) {
   FuseArgs<uint8_t> a = a0;
@@ -558,12 +565,13 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   // ring + barriers + the E(i-1) carry (20 bytes per band per consumer thread)
   const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
                       (size_t)NB * NCW * 32 * 20;
-  auto kern = fuse_d4_u8x8_kernel<NB, NCW>;
+  auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   a.n_colbands = (a.W + CW - 1) / CW;
-  int P = tune.d4_pairs > 0 ? tune.d4_pairs : 32;
+  // 16 row pairs per task (tools/sweep_u8.py: 0.461 ms vs 0.466 at 32)
+  int P = tune.d4_pairs > 0 ? tune.d4_pairs : 16;
   if (P > npairs) P = npairs;
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;
@@ -574,15 +582,18 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
 
 static cudaError_t launch_u8x8(const FuseArgs<uint8_t>& a, cudaStream_t s,
                                const LaunchTuning& tune) {
+  // MS bytes converted on the ALU pipe, PAN bytes on the XU pipe: measured
+  // best of the four splits (0.461 vs 0.473 ms for all-XU on a Landsat scene;
+  // 3 CTAs/SM at 128 registers measured 0.509)
   switch (a.nbands) {
-    case 1: return launch_u8x8_nb<1, 4>(a, s, tune);
-    case 2: return launch_u8x8_nb<2, 4>(a, s, tune);
-    case 3: return launch_u8x8_nb<3, 4>(a, s, tune);
-    case 4: return launch_u8x8_nb<4, 4>(a, s, tune);
-    case 5: return launch_u8x8_nb<5, 4>(a, s, tune);
-    case 6: return launch_u8x8_nb<6, 4>(a, s, tune);
-    case 7: return launch_u8x8_nb<7, 4>(a, s, tune);
-    case 8: return launch_u8x8_nb<8, 4>(a, s, tune);
+    case 1: return launch_u8x8_nb<1, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 2: return launch_u8x8_nb<2, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 3: return launch_u8x8_nb<3, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 4: return launch_u8x8_nb<4, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 5: return launch_u8x8_nb<5, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 6: return launch_u8x8_nb<6, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 7: return launch_u8x8_nb<7, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 8: return launch_u8x8_nb<8, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -28,17 +28,23 @@ def _key(short: str) -> str:
         return "fuse_haar_b" + short.split(",")[2].strip()
     if short.startswith("fuse_d4_tma_kernel<float"):
         return "fuse_daub4_b" + short.split(",")[1].strip()
+    if short.startswith("fuse_d4_u8x8_kernel<"):
+        return "fuse_d4_u8x8_kernel_" + short.split("<")[1].split(",")[0].strip()
     return "".join(c if c.isalnum() else "_" for c in short.replace("wf::", "")).strip("_")
 
 
 def main(reps, tag):
-    out, md = {}, [f"# ncu --set full summary ({tag})", "",
+    """Entries of the given reports replace same-key entries of the existing
+    profiles/ncu_summary.json; the markdown lists every entry."""
+    jp = ROOT / "profiles" / "ncu_summary.json"
+    out = json.loads(jp.read_text()) if jp.exists() else {}
+    md = [f"# ncu --set full summary ({tag})", "",
                    "Captured with `ncu --set full --clock-control none --import-source on`, one "
                    "launch per kernel after warm-up (tools/profile_once.py, profile_u8.py, "
                    "profile_qnr.py). DRAM % is against ncu's own peak.", "",
                    "| kernel | duration | DRAM read | DRAM write | DRAM % of ncu peak | "
-                   "SM % | regs | warps active % | issue IPC |",
-                   "|---|---|---|---|---|---|---|---|---|"]
+                   "SM % | regs | warps active % | issue IPC | report |",
+                   "|---|---|---|---|---|---|---|---|---|---|"]
     for rep in reps:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                              text=True).stdout
@@ -57,14 +63,16 @@ def main(reps, tag):
             rec["kernel"] = short
             rec["report"] = os.path.basename(rep)
             out[_key(short)] = rec
-            md.append(f"| `{short}` | {rec['gpu__time_duration.sum'] * 1e3:.3f} ms | "
-                      f"{rec['dram__bytes_read.sum'] / 1e9:.3f} GB | "
-                      f"{rec['dram__bytes_write.sum'] / 1e9:.3f} GB | "
-                      f"{rec['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
-                      f"{rec['sm__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
-                      f"{rec['launch__registers_per_thread']:.0f} | "
-                      f"{rec['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} | "
-                      f"{rec.get('sm__inst_executed.avg.per_cycle_active') or 0:.2f} |")
+    for rec in out.values():
+        md.append(f"| `{rec['kernel']}` | {rec['gpu__time_duration.sum'] * 1e3:.3f} ms | "
+                  f"{rec['dram__bytes_read.sum'] / 1e9:.3f} GB | "
+                  f"{rec['dram__bytes_write.sum'] / 1e9:.3f} GB | "
+                  f"{rec['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
+                  f"{rec['sm__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
+                  f"{rec['launch__registers_per_thread']:.0f} | "
+                  f"{rec['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} | "
+                  f"{rec.get('sm__inst_executed.avg.per_cycle_active') or 0:.2f} | "
+                  f"{rec['report']} |")
     (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
     (ROOT / "profiles" / f"{tag}_ncu_summary.md").write_text("\n".join(md) + "\n")
     print("\n".join(md))
