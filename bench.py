@@ -218,6 +218,43 @@ def run_reference(args, rank: int):
     print(json.dumps(line), flush=True)
 
 
+_ORIG_AFFINITY: set = set()
+_BOUND: dict = {}
+
+
+def unbind_numa():
+    """All host cores again (the CPU baseline leg uses every core)."""
+    if _ORIG_AFFINITY:
+        os.sched_setaffinity(0, _ORIG_AFFINITY)
+
+
+def bind_numa(dev):
+    """Run this rank on the host cores of its GPU's NUMA node (the PCI
+    device's local_cpulist), before any pinned buffer is allocated, so the
+    e2e leg's pinned staging is node-local to the GPU's PCIe root
+    (WF_BENCH_NUMA=0 disables)."""
+    import torch
+
+    if os.environ.get("WF_BENCH_NUMA", "1") == "0":
+        return None
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        spec = Path(f"/sys/bus/pci/devices/{bus}/local_cpulist").read_text().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            _ORIG_AFFINITY.update(os.sched_getaffinity(0))
+            os.sched_setaffinity(0, cpus)
+            return spec
+    except (OSError, ValueError, AttributeError):
+        pass
+    return None
+
+
 def init_dist(world, local_rank):
     """One process per GPU: rank -> cuda:LOCAL_RANK, NCCL for the timing
     max-reduction and barriers. WF_BENCH_BACKEND=gloo (plumbing checks on a
@@ -229,6 +266,7 @@ def init_dist(world, local_rank):
     backend = os.environ.get("WF_BENCH_BACKEND", "nccl")
     dev = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
     torch.cuda.set_device(dev)
+    _BOUND["cpus"] = bind_numa(dev)
     if world <= 1:
         return None, dev
     import torch.distributed as td
@@ -541,6 +579,7 @@ def run_ours(args, rank, world, local_rank):
     quality = measure_quality(scene, args.steps, args.warmup, peak)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu:
+        unbind_numa()
         threads = os.cpu_count() or 1
         for kname in ("haar", "daub4"):
             rate, t = cpu_sample(kname, args.cpu_rows, threads)
@@ -575,6 +614,7 @@ def run_ours(args, rank, world, local_rank):
                 "bands": B,
                 "parallelism": f"scene-sharded replicas x{world} (no collective)",
                 "l2": "no flush: 2.24 GB of inputs per step >> 126 MB L2",
+                "host_cpus": _BOUND.get("cpus"),
             },
             "gpu_launches": hr["gpu_launches"],
             "clocks": hr["clocks"],
