@@ -461,6 +461,67 @@ def hmean_fuse_ms(scene, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
+def measure_f64(scene, steps, warmup, dist, world, peak):
+    """The same scene as float64 planes -- what a reference caller holding
+    float64 numpy arrays gets (the output dtype follows the PAN,
+    fusion.py:46-47). A step = one PAN-once launch over the whole scene;
+    algorithmic bytes (8 + 10 B) per PAN px. Device-resident only."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind, _native
+    from paper_1803_00737_b200.wavelet import KIND_CODE
+
+    lib = _native.load()
+    h, w = scene.shape
+    pan = scene.pan.double()
+    ms = [m.double() for m in scene.ms]
+    out = [torch.empty((h, w), dtype=torch.float64, device=pan.device) for _ in ms]
+    ms_p = _native.ptr_array([m.data_ptr() for m in ms])
+    out_p = _native.ptr_array([o.data_ptr() for o in out])
+    nbytes = (8 + 10 * len(ms)) * h * w
+    res = {}
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    for kind in (WaveletKind.HAAR, WaveletKind.DAUB4):
+        code = KIND_CODE[kind]
+
+        def run():
+            _native.check(lib.wf_fuse_bands_f64(code, pan.data_ptr(), w, ms_p, w // 2, out_p, w,
+                                                len(ms), h, w, sp))
+
+        for _ in range(warmup):
+            run()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_t = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms_t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_t = float(t.item())
+        per = ms_t / steps
+        achieved = nbytes / (per * 1e-3) / 1e9
+        res[kind.value] = {
+            "value": round(world * h * w / (per * 1e-3) / 1e6, 3),
+            "ms_per_step": round(per, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "kernel": ("fuse_haar_kernel<f64,B=6> (256-bit rows)"
+                                    if kind is WaveletKind.HAAR
+                                    else "fuse_d4_tma_kernel<f64,B=6,4> (256-bit stores)")},
+        }
+    del pan, ms, out
+    torch.cuda.empty_cache()
+    return {"unit": UNIT, "dtype": "f64 in/out, f64 arithmetic", **res}
+
+
 def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
     """the same scene in the paper's 8 bpp transfer
     representation (uint8 in, quantised uint8 out, float32 arithmetic). A
@@ -576,6 +637,7 @@ def run_ours(args, rank, world, local_rank):
             },
         }
     u8 = measure_u8(scene, args.steps, args.warmup, dist, world, local_rank, peak)
+    f64 = measure_f64(scene, args.steps, args.warmup, dist, world, peak)
     quality = measure_quality(scene, args.steps, args.warmup, peak)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -634,6 +696,7 @@ def run_ours(args, rank, world, local_rank):
                 "cpu_baseline": cpu.get("daub4"),
             },
             "u8_8bpp": u8,
+            "f64": f64,
             "quality": quality,
         }
         print(json.dumps(line), flush=True)

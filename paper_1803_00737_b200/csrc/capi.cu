@@ -66,6 +66,7 @@ int check_1d(int kind, int n) {
 }
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool al32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 template <typename T>
 int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, const T* pan_bot,
@@ -137,6 +138,12 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
       if (kind == WF_DAUB4)
         a.ms_top[b] = strip ? ms_top[b0 + b]
                             : ms[b0 + b] + (int64_t)(rows / 2 - 1) * ms_pitch;
+    }
+    // float64: 256-bit row accesses when every row start is 32-byte aligned
+    if (sizeof(T) == 8 && vec && !getenv("WF_NO_WIDE")) {
+      bool w32 = al32(pan) && (pan_pitch * 8) % 32 == 0 && (out_pitch * 8) % 32 == 0;
+      for (int b = 0; b < nb && w32; ++b) w32 = al32(a.out[b]);
+      a.wide = w32 ? 1 : 0;
     }
     bool tma = (allow_tma || sizeof(T) == 1) && kind == WF_DAUB4 && vec && w % (2 * halo) == 0 &&
                row16(pan_pitch) && row16(ms_pitch) && row16(a.halo_pitch) && al16(a.pan_top) &&

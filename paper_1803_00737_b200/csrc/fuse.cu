@@ -278,7 +278,15 @@ __global__ void __launch_bounds__(kHaarThreads)
     const T* r0 = a.pan + (long long)(2 * i) * a.pan_pitch;
     const T* r1 = r0 + a.pan_pitch;
     Acc p0[4], p1[4];
-    if (full) {
+    if constexpr (sizeof(T) == 8 && kVec) {
+      if (a.wide) {
+        load4_wide(r0 + c, p0);
+        load4_wide(r1 + c, p1);
+      } else {
+        load4_vec<Acc>(r0 + c, p0);
+        load4_vec<Acc>(r1 + c, p1);
+      }
+    } else if (full) {
       load4_vec<Acc>(r0 + c, p0);
       load4_vec<Acc>(r1 + c, p1);
     } else {
@@ -306,7 +314,15 @@ __global__ void __launch_bounds__(kHaarThreads)
       Acc o1[4] = {p1[0] + d0, p1[1] + d0, p1[2] + d1, p1[3] + d1};
       T* w0 = a.out[b] + (long long)(2 * i) * a.out_pitch;
       T* w1 = w0 + a.out_pitch;
-      if (full) {
+      if constexpr (sizeof(T) == 8 && kVec) {
+        if (a.wide) {
+          store4_wide(w0 + c, o0);
+          store4_wide(w1 + c, o1);
+        } else {
+          store4_vec<Acc>(w0 + c, o0);
+          store4_vec<Acc>(w1 + c, o1);
+        }
+      } else if (full) {
         store4_vec<Acc>(w0 + c, o0);
         store4_vec<Acc>(w1 + c, o1);
       } else {

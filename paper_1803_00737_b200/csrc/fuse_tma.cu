@@ -110,11 +110,16 @@ __device__ __forceinline__ uint32_t quantize_lanes(float2 v) {
 
 // four consecutive outputs to row-major storage
 template <typename T, typename Acc>
-__device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4]) {
+__device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4], bool wide = false) {
   if constexpr (sizeof(T) == 1) {
     const uint32_t v = __byte_perm(quantize_lanes(make_float2(o[0], o[1])),
                                    quantize_lanes(make_float2(o[2], o[3])), 0x6420);
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else if constexpr (sizeof(T) == 8) {
+    if (wide)
+      store4_wide(p, o);
+    else
+      store4_vec<Acc>(p, o);
   } else {
     store4_vec<Acc>(p, o);
   }
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
                     make_float2(pa[p][2], pa[p][3]),
                     __ffma2_rn(wc, make_float2(v1p, v1p), __fmul2_rn(wp, make_float2(v0p, v0p))));
                 const Acc o[4] = {o01.x, o01.y, o23.x, o23.y};
-                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o, a.wide != 0);
               }
             } else {
 #pragma unroll
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
                 const Acc v1 = fma(wc, e[2], wp * ep[b][2]);
                 const Acc o[4] = {pa[p][0] + fma(h0, v0, h2 * vm), pa[p][1] + fma(h1, v0, h3 * vm),
                                   pa[p][2] + fma(h0, v1, h2 * v0), pa[p][3] + fma(h1, v1, h3 * v0)};
-                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o);
+                if (valid) store4_out<T, Acc>(orow + off0 + (p ? a.out_pitch : 0), o, a.wide != 0);
               }
             }
           }
@@ -622,8 +627,11 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
   // row pairs per CTA: 8 measured best for multi-band f32 on Landsat, longer
   // runs amortise the 2-pair prologue when there is little per-pair work
   // (tools/sweep_d4.py on the Landsat scene: B >= 4 -> 4, B = 2..3 -> 8, B = 1 -> 32)
-  int P = tune.d4_pairs > 0 ? tune.d4_pairs
-                            : (sizeof(T) == 1 ? 32 : (NB == 1 ? 32 : (NB <= 3 ? 8 : 4)));
+  // (float64, 256-bit stores: 16 pairs, 2.36 ms vs 2.45 at 4 -- tools/time_f64.py)
+  int P = tune.d4_pairs > 0
+              ? tune.d4_pairs
+              : (sizeof(T) == 1 ? 32
+                                : (NB == 1 ? 32 : (sizeof(T) == 8 ? 16 : (NB <= 3 ? 8 : 4))));
   if (P > npairs) P = npairs;
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;

@@ -112,6 +112,22 @@ __device__ __forceinline__ void load2_vec(const double* p, Acc (&v)[2]) {
   v[0] = x.x; v[1] = x.y;
 }
 
+// 256-bit forms (LDG/STG.E.ENL2.256, new with sm_100) for float64 rows whose
+// base and pitch are 32-byte aligned: one instruction moves a thread's 4
+// doubles, so each warp instruction covers 1 KB contiguous. The two 128-bit
+// halves of the plain path each cover every other 16 bytes of the warp's span,
+// so every 32-byte sector is written by two separate instructions.
+__device__ __forceinline__ void load4_wide(const double* p, double (&v)[4]) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+}
+__device__ __forceinline__ void store4_wide(double* p, const double (&v)[4]) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]),
+               "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
 template <typename Acc>
 __device__ __forceinline__ void store4_vec(float* p, const Acc (&v)[4]) {
   st_stream(reinterpret_cast<float4*>(p),

@@ -27,6 +27,7 @@ struct FuseArgs {
   T* out[kMaxBandsPerLaunch];
   long long out_pitch;
   int nbands;
+  int wide;  // float64 with 32-byte aligned rows: 256-bit PAN loads / output stores
   int rows;  // PAN rows in this launch (even)
   int W;     // PAN columns (even)
   // filled by the launcher
