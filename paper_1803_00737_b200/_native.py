@@ -72,6 +72,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     sig["wf_fuse_dwt_exact_f32"] = [c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_int, c_int,
                                     c_vp, c_vp]
     sig["wf_fuse_dwt_exact_f64"] = sig["wf_fuse_dwt_exact_f32"]
+    sig["wf_fuse_bands_exact_f32"] = [c_int, c_vp, c_i64, c_vpp, c_i64, c_vpp, c_i64, c_int, c_int,
+                                      c_int, c_vp, c_vp]
+    sig["wf_fuse_bands_exact_f64"] = sig["wf_fuse_bands_exact_f32"]
     for t in ("f32", "f64"):
         sig[f"wf_raster_to_plane_{t}"] = [c_vp, c_int, c_int, c_int, c_int, c_vp, c_i64, c_int,
                                           c_int, c_vp]

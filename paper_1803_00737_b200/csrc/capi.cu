@@ -825,11 +825,34 @@ int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const flo
     cudaError_t e = wf::launch_fuse_exact<T>(kind, pan, pan_pitch, ms, ms_pitch, out,       \
                                              out_pitch, h, w, static_cast<double*>(workspace), \
                                              (cudaStream_t)stream);                          \
-    if (e == cudaSuccess) g_launches += 3;                                                   \
+    if (e == cudaSuccess) g_launches += 2;                                                   \
     return cuda_status(e, #NAME);                                                            \
   }
 WF_FUSE_EXACT(wf_fuse_dwt_exact_f32, float)
 WF_FUSE_EXACT(wf_fuse_dwt_exact_f64, double)
+
+#define WF_FUSE_BANDS_EXACT(NAME, T)                                                        \
+  int NAME(int kind, const T* pan, int64_t pan_pitch, const T* const* ms, int64_t ms_pitch, \
+           T* const* out, int64_t out_pitch, int nbands, int h, int w, void* workspace,      \
+           void* stream) {                                                                   \
+    if (int e = check_kind(kind)) return e;                                                  \
+    if (!pan || !ms || !out || !workspace) return fail(WF_ERR_VALUE, "null pointer argument"); \
+    if (nbands < 1) return fail(WF_ERR_VALUE, "band list is empty");                         \
+    for (int b = 0; b < nbands; ++b)                                                         \
+      if (!ms[b] || !out[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);           \
+    if ((h & 1) || (w & 1))                                                                  \
+      return fail(WF_ERR_ODD_DIMENSION, "panchromatic plane %dx%d has an odd dimension", w, h); \
+    if (h < min_len(kind) || w < min_len(kind))                                              \
+      return fail(WF_ERR_TOO_SMALL, "%dx%d below minimum %d per side", w, h, min_len(kind)); \
+    cudaError_t e = wf::launch_fuse_bands_exact<T>(kind, pan, pan_pitch, ms, ms_pitch, out,  \
+                                                   out_pitch, nbands, h, w,                  \
+                                                   static_cast<double*>(workspace),          \
+                                                   (cudaStream_t)stream);                    \
+    if (e == cudaSuccess) g_launches += 1 + nbands;                                      \
+    return cuda_status(e, #NAME);                                                            \
+  }
+WF_FUSE_BANDS_EXACT(wf_fuse_bands_exact_f32, float)
+WF_FUSE_BANDS_EXACT(wf_fuse_bands_exact_f64, double)
 
 int wf_ipc_export(const void* ptr, void* handle64, uint64_t* offset) {
   if (!ptr || !handle64 || !offset) return fail(WF_ERR_VALUE, "null pointer argument");

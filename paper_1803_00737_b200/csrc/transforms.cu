@@ -44,74 +44,145 @@ __device__ __forceinline__ double inv_tap(int kind, const D4& t, int p, double a
 }
 
 // ---- 2D forward: rows then columns (wavelet.py:149-155) -------------------
-// One thread per coefficient position (i, j) of the half-size grid; it writes
-// LL(i,j), HL(i, Wh+j), LH(Hh+i, j), HH(Hh+i, Wh+j).
-template <typename T, typename To = T>
-__global__ void dwt2d_forward_kernel(int kind, const T* __restrict__ in, long long ip,
-                                     To* __restrict__ out, long long op, int H, int W) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+// A thread owns coefficient column j and marches down a run of kTrRows
+// coefficient rows i. The row pass of PAN rows 2i+2, 2i+3 (wrapped) is
+// carried to row i+1, where it is rows 2i, 2i+1, so every PAN row is loaded,
+// converted and row-filtered once per column instead of twice (D4). It
+// writes LL(i,j), HL(i, Wh+j), LH(Hh+i, j), HH(Hh+i, Wh+j).
+constexpr int kTrThreads = 128;
+constexpr int kTrRows = 8;
+
+template <int KIND, typename T, typename To>
+__global__ void __launch_bounds__(kTrThreads)
+    dwt2d_forward_kernel(const T* __restrict__ in, long long ip, To* __restrict__ out,
+                         long long op, int H, int W) {
+  const int j = blockIdx.x * kTrThreads + threadIdx.x;
   const int Hh = H >> 1, Wh = W >> 1;
-  if (i >= Hh || j >= Wh) return;
+  if (j >= Wh) return;
+  const int i0 = blockIdx.y * kTrRows;
+  const int i1 = min(i0 + kTrRows, Hh);
   const D4 t = d4_taps();
-  const int taps = kind == kHaar ? 2 : 4;
-  double a[4], d[4];
-  for (int k = 0; k < taps; ++k) {
-    const T* row = in + (long long)wrap(2 * i + k, H) * ip;
-    double x[4];
-    for (int l = 0; l < taps; ++l) x[l] = (double)row[wrap(2 * j + l, W)];
-    if (kind == kHaar) x[2] = x[3] = 0.0;
-    a[k] = fwd_lo(kind, t, x[0], x[1], x[2], x[3]);
-    d[k] = fwd_hi(kind, t, x[0], x[1], x[2], x[3]);
+  const int c0 = 2 * j, c1 = 2 * j + 1;
+  const int c2 = KIND == kHaar ? 0 : wrap(2 * j + 2, W), c3 = KIND == kHaar ? 0 : wrap(2 * j + 3, W);
+  auto rowpass = [&](int r, double& a, double& d) {
+    const T* row = in + (long long)r * ip;
+    const double x0 = (double)__ldg(row + c0), x1 = (double)__ldg(row + c1);
+    if (KIND == kHaar) {
+      a = fwd_lo(kHaar, t, x0, x1, 0.0, 0.0);
+      d = fwd_hi(kHaar, t, x0, x1, 0.0, 0.0);
+    } else {
+      const double x2 = (double)__ldg(row + c2), x3 = (double)__ldg(row + c3);
+      a = fwd_lo(kDaub4, t, x0, x1, x2, x3);
+      d = fwd_hi(kDaub4, t, x0, x1, x2, x3);
+    }
+  };
+  auto emit = [&](int i, const double (&a)[4], const double (&d)[4]) {
+    out[(long long)i * op + j] = (To)fwd_lo(KIND, t, a[0], a[1], a[2], a[3]);
+    out[(long long)i * op + Wh + j] = (To)fwd_lo(KIND, t, d[0], d[1], d[2], d[3]);
+    out[(long long)(Hh + i) * op + j] = (To)fwd_hi(KIND, t, a[0], a[1], a[2], a[3]);
+    out[(long long)(Hh + i) * op + Wh + j] = (To)fwd_hi(KIND, t, d[0], d[1], d[2], d[3]);
+  };
+  if (KIND == kHaar) {
+    for (int i = i0; i < i1; ++i) {
+      double a[4] = {0.0, 0.0, 0.0, 0.0}, d[4] = {0.0, 0.0, 0.0, 0.0};
+      rowpass(2 * i, a[0], d[0]);
+      rowpass(2 * i + 1, a[1], d[1]);
+      emit(i, a, d);
+    }
+    return;
   }
-  if (kind == kHaar) a[2] = a[3] = d[2] = d[3] = 0.0;
-  out[(long long)i * op + j] = (To)fwd_lo(kind, t, a[0], a[1], a[2], a[3]);
-  out[(long long)i * op + Wh + j] = (To)fwd_lo(kind, t, d[0], d[1], d[2], d[3]);
-  out[(long long)(Hh + i) * op + j] = (To)fwd_hi(kind, t, a[0], a[1], a[2], a[3]);
-  out[(long long)(Hh + i) * op + Wh + j] = (To)fwd_hi(kind, t, d[0], d[1], d[2], d[3]);
+  double a[4], d[4];
+  rowpass(2 * i0, a[0], d[0]);
+  rowpass(2 * i0 + 1, a[1], d[1]);
+  for (int i = i0; i < i1; ++i) {
+    rowpass(wrap(2 * i + 2, H), a[2], d[2]);
+    rowpass(wrap(2 * i + 3, H), a[3], d[3]);
+    emit(i, a, d);
+    a[0] = a[2];
+    a[1] = a[3];
+    d[0] = d[2];
+    d[1] = d[3];
+  }
 }
 
 // ---- 2D inverse: columns then rows (wavelet.py:158-164) -------------------
-// One thread per output 2x2 block (i, j).
-template <typename T, typename To = T>
-__global__ void dwt2d_inverse_kernel(int kind, const T* __restrict__ in, long long ip,
-                                     To* __restrict__ out, long long op, int H, int W) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+// A thread owns output columns 2j, 2j+1 and marches down coefficient rows i
+// (output rows 2i, 2i+1). The column inverse at coefficient columns
+// {j-1, Wh+j-1, j, Wh+j} needs coefficient rows i-1 and i of both halves;
+// row i-1's values are carried from the previous step, so each coefficient
+// is loaded and converted once per thread.
+// LLMS (reference-exact fusion): the LL quadrant is not read from `in` but
+// formed as band * gain from the MS plane -- the value fusion.py:149 stores
+// there -- so the fused sequence needs no separate LL-replacement pass.
+template <int KIND, typename T, typename To, bool LLMS = false, typename Tm = T>
+__global__ void __launch_bounds__(kTrThreads)
+    dwt2d_inverse_kernel(const T* __restrict__ in, long long ip, To* __restrict__ out,
+                         long long op, int H, int W, const Tm* __restrict__ ms = nullptr,
+                         long long mp = 0, double gain = 1.0) {
+  const int j = blockIdx.x * kTrThreads + threadIdx.x;
   const int Hh = H >> 1, Wh = W >> 1;
-  if (i >= Hh || j >= Wh) return;
+  if (j >= Wh) return;
+  const int i0 = blockIdx.y * kTrRows;
+  const int i1 = min(i0 + kTrRows, Hh);
   const D4 t = d4_taps();
-  const int im = wrap(i - 1, Hh), jm = wrap(j - 1, Wh);
-  // the four coefficient columns the row-inverse of output cols 2j, 2j+1 needs
+  const int jm = wrap(j - 1, Wh);
   const int cols[4] = {jm, Wh + jm, j, Wh + j};
-  double cv[2][4];
-  for (int k = 0; k < 4; ++k) {
-    const int col = cols[k];
-    const double ap = (double)in[(long long)im * ip + col];
-    const double dp = (double)in[(long long)(Hh + im) * ip + col];
-    const double a = (double)in[(long long)i * ip + col];
-    const double d = (double)in[(long long)(Hh + i) * ip + col];
-    cv[0][k] = inv_tap(kind, t, 0, ap, dp, a, d);
-    cv[1][k] = inv_tap(kind, t, 1, ap, dp, a, d);
+  auto load_row = [&](int i, double (&top)[4], double (&bot)[4]) {
+    const T* rt = in + (long long)i * ip;
+    const T* rb = in + (long long)(Hh + i) * ip;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (KIND == kHaar && k < 2) continue;  // Haar reads columns j, Wh+j of row i only
+      if (LLMS && (k & 1) == 0)  // LL(i, col) = band(i, col) * gain
+        top[k] = mul((double)__ldg(ms + (long long)i * mp + cols[k]), gain);
+      else
+        top[k] = (double)__ldg(rt + cols[k]);
+      bot[k] = (double)__ldg(rb + cols[k]);
+    }
+  };
+  double pt[4] = {0.0, 0.0, 0.0, 0.0}, pb[4] = {0.0, 0.0, 0.0, 0.0};  // row i-1
+  if (KIND != kHaar) load_row(wrap(i0 - 1, Hh), pt, pb);
+  for (int i = i0; i < i1; ++i) {
+    double ct[4] = {0.0, 0.0, 0.0, 0.0}, cb[4] = {0.0, 0.0, 0.0, 0.0};
+    load_row(i, ct, cb);
+    double cv[2][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cv[0][k] = inv_tap(KIND, t, 0, pt[k], pb[k], ct[k], cb[k]);
+      cv[1][k] = inv_tap(KIND, t, 1, pt[k], pb[k], ct[k], cb[k]);
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      To* row = out + (long long)(2 * i + p) * op;
+      row[2 * j] = (To)inv_tap(KIND, t, 0, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
+      row[2 * j + 1] = (To)inv_tap(KIND, t, 1, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      pt[k] = ct[k];
+      pb[k] = cb[k];
+    }
   }
-  for (int p = 0; p < 2; ++p) {
-    To* row = out + (long long)(2 * i + p) * op;
-    row[2 * j] = (To)inv_tap(kind, t, 0, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
-    row[2 * j + 1] = (To)inv_tap(kind, t, 1, cv[p][0], cv[p][1], cv[p][2], cv[p][3]);
+}
+
+template <typename T, typename To>
+static void run_dwt2d(int kind, bool inverse, const T* in, long long ip, To* out, long long op,
+                      int h, int w, cudaStream_t s) {
+  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + kTrRows - 1) / kTrRows);
+  if (inverse) {
+    if (kind == kHaar)
+      dwt2d_inverse_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+    else
+      dwt2d_inverse_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+  } else {
+    if (kind == kHaar)
+      dwt2d_forward_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+    else
+      dwt2d_forward_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
   }
 }
 
 // ---- reference-exact fusion (fusion.py:148-150 step by step) ---------------
-// coeffs[:h/2, :w/2] = band.astype(f64) * gain  (fusion.py:149)
-template <typename T>
-__global__ void ll_replace_kernel(double* __restrict__ coeff, long long cp,
-                                  const T* __restrict__ ms, long long mp, int hh, int wh,
-                                  double gain) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= hh || j >= wh) return;
-  coeff[(long long)i * cp + j] = mul((double)ms[(long long)i * mp + j], gain);
-}
 
 // ---- rows-only transforms (dwt1d_* is the nrows = 1 case) ------------------
 template <typename T>
@@ -149,10 +220,19 @@ __global__ void dwt_rows_inverse_kernel(int kind, const T* __restrict__ in, long
 }
 
 // ---- bilinear resample, pixel-centre aligned, clamped (fusion.py:67-81) ----
-__device__ __forceinline__ void src_coord(int dst, int in_n, int out_n, int& i0, int& i1,
+// The source coordinate of a destination index depends on that index alone,
+// so a CTA covers kRsCols destination columns x kRsRows rows: each thread
+// computes its column's (x0, x1, fx) once, the row coordinates are computed
+// once per CTA into shared memory, and the scale in/out is one host-side
+// IEEE division (numpy's `in_w / out_w`) instead of a float64 division per
+// pixel. Same float64 operations in the same order as the reference.
+constexpr int kRsCols = 128;
+constexpr int kRsRows = 16;
+
+__device__ __forceinline__ void src_coord(int dst, double scale, int in_n, int& i0, int& i1,
                                           double& f) {
   // np.clip((arange + 0.5) * (in/out) - 0.5, 0, in-1)
-  double s = sub(mul((double)dst + 0.5, (double)in_n / (double)out_n), 0.5);
+  double s = sub(mul((double)dst + 0.5, scale), 0.5);
   s = fmin(fmax(s, 0.0), (double)(in_n - 1));
   const double fl = floor(s);
   i0 = (int)fl;
@@ -161,21 +241,53 @@ __device__ __forceinline__ void src_coord(int dst, int in_n, int out_n, int& i0,
 }
 
 template <typename T, typename To>
-__global__ void resample_kernel(const T* __restrict__ in, long long ip, int in_h, int in_w,
-                                To* __restrict__ out, long long op, int out_h, int out_w) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= out_w || y >= out_h) return;
-  int x0, x1, y0, y1;
-  double fx, fy;
-  src_coord(x, in_w, out_w, x0, x1, fx);
-  src_coord(y, in_h, out_h, y0, y1, fy);
-  const T* up = in + (long long)y0 * ip;
-  const T* lo = in + (long long)y1 * ip;
-  const double gx = sub(1.0, fx), gy = sub(1.0, fy);
-  const double ru = add(mul((double)up[x0], gx), mul((double)up[x1], fx));
-  const double rl = add(mul((double)lo[x0], gx), mul((double)lo[x1], fx));
-  out[(long long)y * op + x] = (To)add(mul(ru, gy), mul(rl, fy));
+__global__ void __launch_bounds__(kRsCols)
+    resample_kernel(const T* __restrict__ in, long long ip, int in_h, int in_w,
+                    To* __restrict__ out, long long op, int out_h, int out_w, double sx,
+                    double sy) {
+  __shared__ int ry0[kRsRows], ry1[kRsRows];
+  __shared__ double rfy[kRsRows];
+  const int yb = blockIdx.y * kRsRows;
+  if (threadIdx.x < kRsRows && yb + (int)threadIdx.x < out_h) {
+    int a, b;
+    double f;
+    src_coord(yb + threadIdx.x, sy, in_h, a, b, f);
+    ry0[threadIdx.x] = a;
+    ry1[threadIdx.x] = b;
+    rfy[threadIdx.x] = f;
+  }
+  __syncthreads();
+  const int x = blockIdx.x * kRsCols + threadIdx.x;
+  if (x >= out_w) return;
+  int x0, x1;
+  double fx;
+  src_coord(x, sx, in_w, x0, x1, fx);
+  const double gx = sub(1.0, fx);
+  // row_u / row_l of fusion.py:79-80 depend only on (source row, x): the last
+  // two source rows' horizontal interpolants are kept, so when upsampling each
+  // source row is loaded, converted and interpolated once per column instead
+  // of once per output row (the row sequence is uniform across the CTA, so
+  // these branches never diverge)
+  int ca = -1, cb = -1;
+  double ha = 0.0, hb = 0.0;
+  auto hrow = [&](int row) -> double {
+    if (row == ca) return ha;
+    if (row == cb) return hb;
+    const T* p = in + (long long)row * ip;
+    const double v = add(mul((double)__ldg(p + x0), gx), mul((double)__ldg(p + x1), fx));
+    cb = ca;
+    hb = ha;
+    ca = row;
+    ha = v;
+    return v;
+  };
+  const int nr = min(kRsRows, out_h - yb);
+  for (int r = 0; r < nr; ++r) {
+    const double ru = hrow(ry0[r]);
+    const double rl = hrow(ry1[r]);
+    const double fy = rfy[r], gy = sub(1.0, fy);
+    out[(long long)(yb + r) * op + x] = (To)add(mul(ru, gy), mul(rl, fy));
+  }
 }
 
 // ---- counter-hash synthetic planes -----------------------------------------
@@ -253,12 +365,7 @@ template cudaError_t launch_quantize<double>(const double*, long long, int, int,
 template <typename T>
 cudaError_t launch_dwt2d(int kind, bool inverse, const T* in, long long ip, T* out,
                          long long op, int h, int w, cudaStream_t s) {
-  dim3 block(32, 8);
-  dim3 grid(((w >> 1) + 31) / 32, ((h >> 1) + 7) / 8);
-  if (inverse)
-    dwt2d_inverse_kernel<T><<<grid, block, 0, s>>>(kind, in, ip, out, op, h, w);
-  else
-    dwt2d_forward_kernel<T><<<grid, block, 0, s>>>(kind, in, ip, out, op, h, w);
+  run_dwt2d<T, T>(kind, inverse, in, ip, out, op, h, w, s);
   return cudaGetLastError();
 }
 
@@ -276,9 +383,10 @@ cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long ip, T
 template <typename T, typename To>
 cudaError_t launch_resample(const T* in, long long ip, int in_h, int in_w, To* out, long long op,
                             int out_h, int out_w, cudaStream_t s) {
-  dim3 block(32, 8);
-  dim3 grid((out_w + 31) / 32, (out_h + 7) / 8);
-  resample_kernel<T, To><<<grid, block, 0, s>>>(in, ip, in_h, in_w, out, op, out_h, out_w);
+  dim3 grid((out_w + kRsCols - 1) / kRsCols, (out_h + kRsRows - 1) / kRsRows);
+  resample_kernel<T, To><<<grid, kRsCols, 0, s>>>(in, ip, in_h, in_w, out, op, out_h, out_w,
+                                                   (double)in_w / (double)out_w,
+                                                   (double)in_h / (double)out_h);
   return cudaGetLastError();
 }
 
@@ -289,20 +397,47 @@ cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsign
   return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
+                                    long long mp, T* const* out, long long op, int nbands,
+                                    int h, int w, double* ws, cudaStream_t s);
+
 // fuse_dwt exactly as the reference computes it: float64 forward transform
 // of the PAN plane (its exact operation order), LL <- band * gain, float64
 // inverse, one final cast to the PAN dtype. `ws` = h * w doubles.
 template <typename T>
 cudaError_t launch_fuse_exact(int kind, const T* pan, long long pp, const T* ms, long long mp,
                               T* out, long long op, int h, int w, double* ws, cudaStream_t s) {
-  dim3 block(32, 8);
-  dim3 grid(((w >> 1) + 31) / 32, ((h >> 1) + 7) / 8);
-  dwt2d_forward_kernel<T, double><<<grid, block, 0, s>>>(kind, pan, pp, ws, w, h, w);
-  ll_replace_kernel<T><<<grid, block, 0, s>>>(ws, w, ms, mp, h >> 1, w >> 1,
-                                              kind == kHaar ? 1.0 : 2.0);
-  dwt2d_inverse_kernel<double, T><<<grid, block, 0, s>>>(kind, ws, w, out, op, h, w);
+  return launch_fuse_bands_exact<T>(kind, pan, pp, &ms, mp, &out, op, 1, h, w, ws, s);
+}
+// fuse() in the exact sequence for all bands: forward once, then per band
+// LL <- band * gain and the inverse (the detail quadrants of ws stay as the
+// forward pass left them; LL is fully overwritten per band).
+template <typename T>
+cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
+                                    long long mp, T* const* out, long long op, int nbands,
+                                    int h, int w, double* ws, cudaStream_t s) {
+  run_dwt2d<T, double>(kind, false, pan, pp, ws, w, h, w, s);
+  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + kTrRows - 1) / kTrRows);
+  for (int b = 0; b < nbands; ++b) {
+    if (kind == kHaar)
+      dwt2d_inverse_kernel<kHaar, double, T, true, T>
+          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, ms[b], mp, 1.0);
+    else
+      dwt2d_inverse_kernel<kDaub4, double, T, true, T>
+          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, ms[b], mp, 2.0);
+  }
   return cudaGetLastError();
 }
+template cudaError_t launch_fuse_bands_exact<float>(int, const float*, long long,
+                                                    const float* const*, long long, float* const*,
+                                                    long long, int, int, int, double*,
+                                                    cudaStream_t);
+template cudaError_t launch_fuse_bands_exact<double>(int, const double*, long long,
+                                                     const double* const*, long long,
+                                                     double* const*, long long, int, int, int,
+                                                     double*, cudaStream_t);
+
 template cudaError_t launch_fuse_exact<float>(int, const float*, long long, const float*,
                                               long long, float*, long long, int, int, double*,
                                               cudaStream_t);

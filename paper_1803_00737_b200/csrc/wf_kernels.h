@@ -87,6 +87,10 @@ cudaError_t launch_dwt_rows(int kind, bool inverse, const T* in, long long in_pi
 template <typename T>
 cudaError_t launch_fuse_exact(int kind, const T* pan, long long pp, const T* ms, long long mp,
                               T* out, long long op, int h, int w, double* ws, cudaStream_t s);
+template <typename T>
+cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
+                                    long long mp, T* const* out, long long op, int nbands,
+                                    int h, int w, double* ws, cudaStream_t s);
 
 // fusion.py:50-81
 template <typename T, typename To>

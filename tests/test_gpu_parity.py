@@ -401,3 +401,37 @@ def test_exact_mode_bit_identical_to_reference(golden_fusion, kname):
             ref = g[f"{name}/{kname}/out{b}"]
             assert o.dtype == ref.dtype
             assert np.array_equal(o, ref), (name, kname, b, _maxabs(o, ref))
+
+
+@pytest.mark.parametrize("src,dst", [((300, 517), (1000, 777)), ((1000, 777), (123, 456)),
+                                     ((7, 9), (40, 33)), ((64, 64), (128, 128))])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_resample_bilinear_larger_vs_oracle(src, dst, dt):
+    """Up- and down-sampling across several CTA rows/columns of the resample
+    kernel (partial edge tiles), bit-identical to the reference's float64
+    sequence (fusion.py:67-81) via the pinned oracle."""
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0, 255, src).astype(dt)
+    got = wf.resample_bilinear(x, dst[1], dst[0])
+    ref = O.resample_bilinear(x, dst[1], dst[0])
+    assert got.dtype == ref.dtype
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_exact_mode_multi_cta_vs_oracle(kname, dt):
+    """The exact path on a plane spanning many CTAs of the marching
+    transform kernels (partial row runs and column blocks; the PAN forward
+    transform shared by all bands, LL formed from the band inside the
+    inverse) equals the pinned float64 oracle bit for bit."""
+    rng = np.random.default_rng(21)
+    pan = rng.uniform(0, 255, (148, 1048)).astype(dt)
+    bands = [rng.uniform(0, 255, (74, 524)).astype(dt) for _ in range(3)]
+    got = wf.fuse(pan, bands, wf.DwtReplace(KINDS[kname]), exact=True)
+    ref = O.fuse(pan, bands, kname)
+    for o, r in zip(got, ref):
+        assert o.dtype == r.dtype
+        assert np.array_equal(o, r)
+    one = wf.fuse_dwt(pan, bands[1], KINDS[kname], exact=True)
+    assert np.array_equal(one, got[1])
