@@ -827,9 +827,14 @@ def run_batch(args, rank, world, local_rank):
     reports = []
 
     def step(record):
+        # every pass queued back to back; the reports' scalars are read once
+        # per step (qnr_async), so the GPU never idles on a per-scene sync
+        pending = []
         for sc, run in runs:
             run()
-            rep = wf.qnr(sc.out, sc.ms, sc.pan)
+            pending.append(wf.qnr_async(sc.out, sc.ms, sc.pan))
+        for p in pending:
+            rep = p.result()
             if record:
                 reports.append(rep.qnr)
 

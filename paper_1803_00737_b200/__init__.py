@@ -37,7 +37,8 @@ from .fusion import (
     quantize,
     resample_bilinear,
 )
-from .metrics import QualityReport, d_lambda, d_s, degrade, ergas, fuse_and_qnr, q_index, qnr
+from .metrics import (PendingReport, QualityReport, d_lambda, d_s, degrade, ergas, fuse_and_qnr,
+                      q_index, qnr, qnr_async)
 from .pnm import PnmRaster, fuse_pnm, read_pnm, to_plane, write_pnm
 from .tiling import TileGrid, fuse_tiled, pad_edge, pad_inputs, padded_dims, plan_grid
 from .wavelet import (
@@ -100,6 +101,8 @@ __all__ = [
     "plan_grid",
     "q_index",
     "qnr",
+    "qnr_async",
+    "PendingReport",
     "quantize",
     "read_pnm",
     "resample_bilinear",

@@ -589,7 +589,8 @@ static cudaError_t launch_u8x8(const FuseArgs<uint8_t>& a, cudaStream_t s,
                                const LaunchTuning& tune) {
   // MS bytes converted on the ALU pipe, PAN bytes on the XU pipe: measured
   // best of the four splits (0.461 vs 0.473 ms for all-XU on a Landsat scene;
-  // 3 CTAs/SM at 128 registers measured 0.509)
+  // 3 CTAs/SM at 128 registers measured 0.509, 5 CTAs/SM at 72 registers
+  // spill and measured 0.510)
   switch (a.nbands) {
     case 1: return launch_u8x8_nb<1, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
     case 2: return launch_u8x8_nb<2, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
