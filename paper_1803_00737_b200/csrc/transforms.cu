@@ -13,6 +13,8 @@
 // h3*odd1` (wavelet.py:85) as ((h0*e + h1*o) + h2*e1) + h3*o1 with each
 // operation correctly rounded; so does this file, so results are
 // bit-identical to the reference (tests/test_gpu_parity.py checks equality).
+#include <stdlib.h>
+
 #include "wf_common.cuh"
 #include "wf_kernels.h"
 
@@ -50,17 +52,26 @@ __device__ __forceinline__ double inv_tap(int kind, const D4& t, int p, double a
 // converted and row-filtered once per column instead of twice (D4). It
 // writes LL(i,j), HL(i, Wh+j), LH(Hh+i, j), HH(Hh+i, Wh+j).
 constexpr int kTrThreads = 128;
-constexpr int kTrRows = 8;
+constexpr int kTrRowsDefault = 8;
+// coefficient rows per thread (WF_TR_ROWS overrides, for sweeps)
+static int tr_rows() {
+  static int r = [] {
+    const char* e = getenv("WF_TR_ROWS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : kTrRowsDefault;
+  }();
+  return r;
+}
 
 template <int KIND, typename T, typename To>
 __global__ void __launch_bounds__(kTrThreads)
     dwt2d_forward_kernel(const T* __restrict__ in, long long ip, To* __restrict__ out,
-                         long long op, int H, int W) {
+                         long long op, int H, int W, int rows) {
   const int j = blockIdx.x * kTrThreads + threadIdx.x;
   const int Hh = H >> 1, Wh = W >> 1;
   if (j >= Wh) return;
-  const int i0 = blockIdx.y * kTrRows;
-  const int i1 = min(i0 + kTrRows, Hh);
+  const int i0 = blockIdx.y * rows;
+  const int i1 = min(i0 + rows, Hh);
   const D4 t = d4_taps();
   const int c0 = 2 * j, c1 = 2 * j + 1;
   const int c2 = KIND == kHaar ? 0 : wrap(2 * j + 2, W), c3 = KIND == kHaar ? 0 : wrap(2 * j + 3, W);
@@ -117,13 +128,13 @@ __global__ void __launch_bounds__(kTrThreads)
 template <int KIND, typename T, typename To, bool LLMS = false, typename Tm = T>
 __global__ void __launch_bounds__(kTrThreads)
     dwt2d_inverse_kernel(const T* __restrict__ in, long long ip, To* __restrict__ out,
-                         long long op, int H, int W, const Tm* __restrict__ ms = nullptr,
+                         long long op, int H, int W, int rows, const Tm* __restrict__ ms = nullptr,
                          long long mp = 0, double gain = 1.0) {
   const int j = blockIdx.x * kTrThreads + threadIdx.x;
   const int Hh = H >> 1, Wh = W >> 1;
   if (j >= Wh) return;
-  const int i0 = blockIdx.y * kTrRows;
-  const int i1 = min(i0 + kTrRows, Hh);
+  const int i0 = blockIdx.y * rows;
+  const int i1 = min(i0 + rows, Hh);
   const D4 t = d4_taps();
   const int jm = wrap(j - 1, Wh);
   const int cols[4] = {jm, Wh + jm, j, Wh + j};
@@ -168,17 +179,17 @@ __global__ void __launch_bounds__(kTrThreads)
 template <typename T, typename To>
 static void run_dwt2d(int kind, bool inverse, const T* in, long long ip, To* out, long long op,
                       int h, int w, cudaStream_t s) {
-  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + kTrRows - 1) / kTrRows);
+  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + tr_rows() - 1) / tr_rows());
   if (inverse) {
     if (kind == kHaar)
-      dwt2d_inverse_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+      dwt2d_inverse_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w, tr_rows());
     else
-      dwt2d_inverse_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+      dwt2d_inverse_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w, tr_rows());
   } else {
     if (kind == kHaar)
-      dwt2d_forward_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+      dwt2d_forward_kernel<kHaar, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w, tr_rows());
     else
-      dwt2d_forward_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w);
+      dwt2d_forward_kernel<kDaub4, T, To><<<grid, kTrThreads, 0, s>>>(in, ip, out, op, h, w, tr_rows());
   }
 }
 
@@ -418,14 +429,14 @@ cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const 
                                     long long mp, T* const* out, long long op, int nbands,
                                     int h, int w, double* ws, cudaStream_t s) {
   run_dwt2d<T, double>(kind, false, pan, pp, ws, w, h, w, s);
-  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + kTrRows - 1) / kTrRows);
+  dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + tr_rows() - 1) / tr_rows());
   for (int b = 0; b < nbands; ++b) {
     if (kind == kHaar)
       dwt2d_inverse_kernel<kHaar, double, T, true, T>
-          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, ms[b], mp, 1.0);
+          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, tr_rows(), ms[b], mp, 1.0);
     else
       dwt2d_inverse_kernel<kDaub4, double, T, true, T>
-          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, ms[b], mp, 2.0);
+          <<<grid, kTrThreads, 0, s>>>(ws, w, out[b], op, h, w, tr_rows(), ms[b], mp, 2.0);
   }
   return cudaGetLastError();
 }
