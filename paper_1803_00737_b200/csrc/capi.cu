@@ -782,7 +782,7 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
   cudaError_t e = wf::launch_quality_scene(nbands, fused, ms, pan, f_pitch, ms_pitch, pan_pitch,
                                            h, w, workspace, out, undecidable,
                                            (cudaStream_t)stream);
-  if (e == cudaSuccess) g_launches += 3;
+  if (e == cudaSuccess) g_launches += 4;  // scene kernel, edge, two finish levels
   return cuda_status(e, "wf_quality_scene_f32");
 }
 
@@ -809,7 +809,7 @@ int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const flo
   cudaError_t e = wf::launch_fuse_quality_haar(nbands, pan, ms, out, out_pitch, ms_pitch,
                                                pan_pitch, h, w, workspace, report, undecidable,
                                                (cudaStream_t)stream);
-  if (e == cudaSuccess) g_launches += 5;
+  if (e == cudaSuccess) g_launches += 6;
   return cuda_status(e, "wf_fuse_quality_f32");
 }
 

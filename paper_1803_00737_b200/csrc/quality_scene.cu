@@ -595,33 +595,46 @@ __global__ void __launch_bounds__(256)
 
 // out layout: [NQ block-mean Q values] [NB low-res Q(M_k, Pd) means]
 //             [NB MSE_k] [NB mean(M_k)]
-// One CTA per output quantity; each reduces its column in a fixed order
-// (deterministic), so the finish costs microseconds, not a serial sweep.
+// Two deterministic levels: CTA (q, split) sums the split-th contiguous chunk
+// of quantity q's column into fin[q][split] (thread-strided in a fixed order,
+// then a fixed-order block sum); quality_finish2_kernel adds the kFinSplit
+// partials of each quantity in order and normalises. 60 quantities x 16
+// chunks spread the ~100 MB of partials over the whole chip (one CTA per
+// quantity left most SMs idle).
+constexpr int kFinSplit = 16;
+constexpr int kFinThreads = 256;
+
 template <int NB>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kFinThreads)
     quality_finish_kernel(const QsArgs a, const double* part_q, int ncta, const double* part_low,
                           const double* part_erg, const double* part_edge, int nedge,
-                          double* out, int* undecidable) {
+                          double* fin, int* undecidable) {
   using L = QsLayout<NB>;
-  __shared__ double red[32];
+  __shared__ double red[kFinThreads / 32];
   auto block_sum = [&](double v) {
     v = warp_sum_d(v);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    for (int w = 0; w < kFinThreads / 32; ++w) t += red[w];
     return t;
+  };
+  auto chunk = [&](int n, int& lo, int& hi) {
+    const int per = (n + kFinSplit - 1) / kFinSplit;
+    lo = min(n, (int)blockIdx.y * per);
+    hi = min(n, lo + per);
   };
   const int q = blockIdx.x;
   double v = 0.0;
+  int lo, hi;
   if (q < L::NQ) {
-    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_q[(size_t)q * ncta + c];
-    v = block_sum(v);
-    if (threadIdx.x == 0) out[q] = v / ((double)a.nbr * a.nbc);
+    chunk(ncta, lo, hi);
+    for (int c = lo + threadIdx.x; c < hi; c += kFinThreads) v += part_q[(size_t)q * ncta + c];
   } else if (q < L::NQ + NB) {
     const int k = q - L::NQ;
     const int nlow = a.nbr_l * a.nbc_l;
-    for (int b = threadIdx.x; b < nlow; b += blockDim.x) {
+    chunk(nlow, lo, hi);
+    for (int b = lo + threadIdx.x; b < hi; b += kFinThreads) {
       const size_t nl = (size_t)nlow, qs = (size_t)(L::NLOW + NB + 1) * nl;
       const double* src = part_low + b;
       double s1m = 0, s1p = 0, smm = 0, spp = 0, smp = 0;
@@ -636,15 +649,27 @@ __global__ void __launch_bounds__(1024)
       v += q_from_sums(1024.0, src[(L::NLOW + k) * nl], src[(L::NLOW + NB) * nl], s1m, s1p, smm, spp, smp,
                        undecidable);
     }
-    v = block_sum(v);
-    if (threadIdx.x == 0) out[q] = v / (double)nlow;
   } else {
     const int e = q - L::NQ - NB;  // 0..2NB-1: sse_k then sum_k
-    for (int c = threadIdx.x; c < ncta; c += blockDim.x) v += part_erg[(size_t)e * ncta + c];
-    for (int c = threadIdx.x; c < nedge; c += blockDim.x) v += part_edge[(size_t)e * nedge + c];
-    v = block_sum(v);
-    if (threadIdx.x == 0) out[q] = v / ((double)a.Hh * a.Wh);
+    chunk(ncta, lo, hi);
+    for (int c = lo + threadIdx.x; c < hi; c += kFinThreads) v += part_erg[(size_t)e * ncta + c];
+    if (blockIdx.y == 0)
+      for (int c = threadIdx.x; c < nedge; c += kFinThreads) v += part_edge[(size_t)e * nedge + c];
   }
+  v = block_sum(v);
+  if (threadIdx.x == 0) fin[(size_t)q * kFinSplit + blockIdx.y] = v;
+}
+
+template <int NB>
+__global__ void quality_finish2_kernel(const QsArgs a, const double* fin, double* out) {
+  using L = QsLayout<NB>;
+  const int q = threadIdx.x;
+  if (q >= L::NQ + 3 * NB) return;
+  double v = 0.0;
+  for (int i = 0; i < kFinSplit; ++i) v += fin[(size_t)q * kFinSplit + i];
+  const double n = q < L::NQ ? (double)a.nbr * a.nbc
+                             : q < L::NQ + NB ? (double)a.nbr_l * a.nbc_l : (double)a.Hh * a.Wh;
+  out[q] = v / n;
 }
 
 // ---------------------------------------------------------------------------
@@ -1451,7 +1476,8 @@ static size_t qs_workspace_nb(int h, int w) {
   // v2 writes one partial per block column of a tile (>= v1's one per tile)
   const size_t ncta = (size_t)nbr * ncx * kQ2Bc;
   return sizeof(double) * (ncta * L::NQ + (size_t)nbr_l * nbc_l * 4 * (L::NLOW + NB + 1) +
-                           ncta * L::NERG + (size_t)kEdgeCtas * 2 * NB) +
+                           ncta * L::NERG + (size_t)kEdgeCtas * 2 * NB +
+                           (size_t)(L::NQ + 3 * NB) * kFinSplit) +
          64;
 }
 
@@ -1530,6 +1556,7 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   double* part_low = part_q + (size_t)nparts * L::NQ;
   double* part_erg = part_low + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
   double* part_edge = part_erg + (size_t)nparts * L::NERG;
+  double* fin = part_edge + (size_t)kEdgeCtas * 2 * NB;
   Q2Maps maps;
   if (!v1) {
     // the role-split kernel needs tensor maps; 16-byte strides (W % 4 == 0)
@@ -1576,8 +1603,10 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
     quality_edge_kernel<NB><<<nedge, 256, 0, s>>>(a, row_lo, col_lo, part_edge);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  quality_finish_kernel<NB><<<L::NQ + 3 * NB, 1024, 0, s>>>(a, part_q, nparts, part_low, part_erg,
-                                                            part_edge, nedge, out, undecidable);
+  quality_finish_kernel<NB><<<dim3(L::NQ + 3 * NB, kFinSplit), kFinThreads, 0, s>>>(
+      a, part_q, nparts, part_low, part_erg, part_edge, nedge, fin, undecidable);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  quality_finish2_kernel<NB><<<1, 128, 0, s>>>(a, fin, out);
   return cudaGetLastError();
 }
 
