@@ -513,6 +513,9 @@ def measure_f64(scene, steps, warmup, dist, world, peak):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_launch": nbytes,
+                         "traffic": ncu_traffic("fuse_haar_kernel_double__double__6__1__1"
+                                                if kind is WaveletKind.HAAR
+                                                else "fuse_d4_tma_kernel_double__6__4"),
                          "kernel": ("fuse_haar_kernel<f64,B=6> (256-bit rows)"
                                     if kind is WaveletKind.HAAR
                                     else "fuse_d4_tma_kernel<f64,B=6,4> (256-bit stores)")},
