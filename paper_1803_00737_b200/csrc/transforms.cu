@@ -408,6 +408,312 @@ cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsign
   return cudaGetLastError();
 }
 
+// ---- reference-exact Haar fusion in one pass --------------------------------
+// Every Haar coefficient is 2x2-local, so fusion.py:148-150 for all bands runs
+// in one kernel with no coefficient image: a thread owns PAN columns
+// 4q..4q+3 of one row pair, forms that row pair's detail coefficients with
+// the reference's float64 operations (wavelet.py:75-86 rows, then columns:
+// LH = (a0 - a1) * 0.5, HL = (d0 + d1) * 0.5, HH = (d0 - d1) * 0.5), and per
+// band sets LL = band (gain 1, fusion.py:125) and runs the inverse (columns:
+// cvA = LL +/- LH, cvD = HL +/- HH; rows: out = cvA +/- cvD, wavelet.py:96-108)
+// before one cast to the PAN dtype. Same operations, same order: bit-identical
+// to the transform path.
+struct ExactBands {
+  const void* ms[kMaxBandsPerLaunch];
+  void* out[kMaxBandsPerLaunch];
+};
+
+template <typename T, int NB, bool kVec>
+__global__ void __launch_bounds__(128)
+    fuse_exact_haar_kernel(const T* __restrict__ pan, long long pp, const ExactBands bands,
+                           long long mp, long long op, int H, int W) {
+  const int q = blockIdx.x * 128 + threadIdx.x;
+  const int i = blockIdx.y;  // coefficient row = PAN row pair
+  const int c4 = 4 * q;
+  if (c4 >= W) return;
+  const int ncol = min(4, W - c4);  // 2 or 4 (W even)
+  const T* r0 = pan + (long long)(2 * i) * pp + c4;
+  const T* r1 = r0 + pp;
+  double x[2][4];
+  if (kVec && sizeof(T) == 8 && ((reinterpret_cast<uintptr_t>(r0) | pp * 8) & 31) == 0) {
+    load4_wide(reinterpret_cast<const double*>(r0), x[0]);
+    load4_wide(reinterpret_cast<const double*>(r1), x[1]);
+  } else if (kVec) {
+    double v[4];
+    load4_vec<double>(r0, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[0][k] = v[k];
+    load4_vec<double>(r1, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[1][k] = v[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[0][k] = k < ncol ? (double)__ldg(r0 + k) : 0.0;
+      x[1][k] = k < ncol ? (double)__ldg(r1 + k) : 0.0;
+    }
+  }
+  double lh[2], cvd[2][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    double a[2], d[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      a[r] = fwd_lo(kHaar, D4{}, x[r][2 * c], x[r][2 * c + 1], 0.0, 0.0);
+      d[r] = fwd_hi(kHaar, D4{}, x[r][2 * c], x[r][2 * c + 1], 0.0, 0.0);
+    }
+    lh[c] = fwd_hi(kHaar, D4{}, a[0], a[1], 0.0, 0.0);
+    const double hl = fwd_lo(kHaar, D4{}, d[0], d[1], 0.0, 0.0);
+    const double hh = fwd_hi(kHaar, D4{}, d[0], d[1], 0.0, 0.0);
+    cvd[0][c] = add(hl, hh);
+    cvd[1][c] = sub(hl, hh);
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const T* m = static_cast<const T*>(bands.ms[b]) + (long long)i * mp + 2 * q;
+    double ll[2];
+    ll[0] = (double)__ldg(m);
+    ll[1] = ncol > 2 ? (double)__ldg(m + 1) : 0.0;
+    double o[2][4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const double cva = p == 0 ? add(ll[c], lh[c]) : sub(ll[c], lh[c]);
+        o[p][2 * c] = add(cva, cvd[p][c]);
+        o[p][2 * c + 1] = sub(cva, cvd[p][c]);
+      }
+    T* w0 = static_cast<T*>(bands.out[b]) + (long long)(2 * i) * op + c4;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      T* w = w0 + (p ? op : 0);
+      if (kVec && sizeof(T) == 8 && ((reinterpret_cast<uintptr_t>(w) | op * 8) & 31) == 0) {
+        store4_wide(reinterpret_cast<double*>(w), o[p]);
+      } else if (kVec) {
+        store4_vec<double>(w, o[p]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < ncol) w[k] = (T)o[p][k];
+      }
+    }
+  }
+}
+
+template <typename T, int NB>
+static void launch_exact_haar_nb(const T* pan, long long pp, const ExactBands& eb, long long mp,
+                                 long long op, int h, int w, bool vec, cudaStream_t s) {
+  dim3 grid(((w + 3) / 4 + 127) / 128, h >> 1);
+  if (vec)
+    fuse_exact_haar_kernel<T, NB, true><<<grid, 128, 0, s>>>(pan, pp, eb, mp, op, h, w);
+  else
+    fuse_exact_haar_kernel<T, NB, false><<<grid, 128, 0, s>>>(pan, pp, eb, mp, op, h, w);
+}
+
+template <typename T>
+static cudaError_t launch_exact_haar(const T* pan, long long pp, const T* const* ms, long long mp,
+                                     T* const* out, long long op, int nbands, int h, int w,
+                                     cudaStream_t s) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
+    const int nb = min(kMaxBandsPerLaunch, nbands - b0);
+    ExactBands eb{};
+    bool vec = w % 4 == 0 && al16(pan) && (pp * (long long)sizeof(T)) % 16 == 0 &&
+               (op * (long long)sizeof(T)) % 16 == 0;
+    for (int b = 0; b < nb; ++b) {
+      eb.ms[b] = ms[b0 + b];
+      eb.out[b] = out[b0 + b];
+      vec = vec && al16(out[b0 + b]);
+    }
+    switch (nb) {
+#define WF_EH(N) \
+  case N: launch_exact_haar_nb<T, N>(pan, pp, eb, mp, op, h, w, vec, s); break;
+      WF_EH(1) WF_EH(2) WF_EH(3) WF_EH(4) WF_EH(5) WF_EH(6) WF_EH(7) WF_EH(8)
+#undef WF_EH
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return cudaGetLastError();
+}
+
+// ---- reference-exact D4 fusion in one pass ----------------------------------
+// fusion.py:148-150 for all bands with no coefficient image. A thread owns
+// coefficient column j (output columns 2j, 2j+1) and marches down a run of
+// coefficient rows i. Output rows 2i, 2i+1 need, at coefficient columns
+// jm = j-1 and j (wrapped) and rows i-1 and i, the detail coefficients LH,
+// HL, HH of the PAN and LL = band * 2 (fusion.py:125,149). The forward pass is
+// the reference's own (wavelet.py:75-86: rows of PAN rows 2i+2, 2i+3, then
+// columns), carried down the run; the inverse (wavelet.py:96-108) is split
+// into the products that only involve PAN coefficients -- formed once per row
+// step -- and the band terms, added in the reference's order per band:
+//   cvA = ((hp2*LL(i-1) + gp2*LH(i-1)) + hp0*LL(i)) + gp0*LH(i)
+//   cvD = ((hp2*HL(i-1) + gp2*HH(i-1)) + hp0*HL(i)) + gp0*HH(i)
+//   out(2i+p, 2j+e) = ((he2*cvA(jm) + ge2*cvD(jm)) + he0*cvA(j)) + ge0*cvD(j)
+// with every product and sum rounded separately (no FMA), one final cast:
+// bit-identical to the transform path.
+constexpr int kExactRows = 16;
+
+template <typename T, int NB, bool kVec>
+__global__ void __launch_bounds__(128)
+    fuse_exact_d4_kernel(const T* __restrict__ pan, long long pp, const ExactBands bands,
+                         long long mp, long long op, int H, int W, int rows) {
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const int Hh = H >> 1, Wh = W >> 1;
+  if (j >= Wh) return;
+  const int i0 = blockIdx.y * rows;
+  const int i1 = min(i0 + rows, Hh);
+  const D4 t = d4_taps();
+  const int jm = wrap(j - 1, Wh);
+  // PAN columns 2jm .. 2jm+3 and 2j .. 2j+3 (wrapped): 2j-2 .. 2j+3
+  int col[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) col[k] = wrap(2 * j - 2 + k, W);
+  // row pass of one PAN row at coefficient columns jm (c = 0) and j (c = 1)
+  auto rowpass = [&](int r, double (&a)[2], double (&d)[2]) {
+    const T* row = pan + (long long)r * pp;
+    double x[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) x[k] = (double)__ldg(row + col[k]);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      a[c] = fwd_lo(kDaub4, t, x[2 * c], x[2 * c + 1], x[2 * c + 2], x[2 * c + 3]);
+      d[c] = fwd_hi(kDaub4, t, x[2 * c], x[2 * c + 1], x[2 * c + 2], x[2 * c + 3]);
+    }
+  };
+  // column pass of coefficient row i from the row passes of PAN rows 2i..2i+3
+  auto colpass = [&](const double (&a)[4][2], const double (&d)[4][2], double (&lh)[2],
+                     double (&hl)[2], double (&hh)[2]) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      lh[c] = fwd_hi(kDaub4, t, a[0][c], a[1][c], a[2][c], a[3][c]);
+      hl[c] = fwd_lo(kDaub4, t, d[0][c], d[1][c], d[2][c], d[3][c]);
+      hh[c] = fwd_hi(kDaub4, t, d[0][c], d[1][c], d[2][c], d[3][c]);
+    }
+  };
+  // synthesis taps (wavelet.py:96-108): parity p -> (hp2, gp2, hp0, gp0)
+  const double sh2[2] = {t.h2, t.h3}, sg2[2] = {t.g2, t.g3};
+  const double sh0[2] = {t.h0, t.h1}, sg0[2] = {t.g0, t.g1};
+
+  double a[4][2], d[4][2];  // row passes of PAN rows 2i .. 2i+3
+  double lhp[2], hlp[2], hhp[2];  // detail coefficients of row i-1
+  {
+    const int im = wrap(i0 - 1, Hh);
+    rowpass(2 * im, a[0], d[0]);
+    rowpass(2 * im + 1, a[1], d[1]);
+    rowpass(2 * i0, a[2], d[2]);
+    rowpass(2 * i0 + 1, a[3], d[3]);
+    colpass(a, d, lhp, hlp, hhp);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      a[0][c] = a[2][c];
+      a[1][c] = a[3][c];
+      d[0][c] = d[2][c];
+      d[1][c] = d[3][c];
+    }
+  }
+  for (int i = i0; i < i1; ++i) {
+    rowpass(wrap(2 * i + 2, H), a[2], d[2]);
+    rowpass(wrap(2 * i + 3, H), a[3], d[3]);
+    double lh[2], hl[2], hh[2];
+    colpass(a, d, lh, hl, hh);
+    // PAN-only parts of the inverse
+    double qa0[2][2], qa1[2][2], qd[2][4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      double cvd[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        cvd[c] = add(add(add(mul(sh2[p], hlp[c]), mul(sg2[p], hhp[c])), mul(sh0[p], hl[c])),
+                     mul(sg0[p], hh[c]));
+        qa0[p][c] = mul(sg2[p], lhp[c]);
+        qa1[p][c] = mul(sg0[p], lh[c]);
+      }
+      // output column parity e: (he2, ge2, he0, ge0) applied to (cvA(jm), cvD(jm), cvA(j), cvD(j))
+      qd[p][0] = mul(sg2[0], cvd[0]);  // e = 0: g2 * cvD(jm)
+      qd[p][1] = mul(sg0[0], cvd[1]);  //        g0 * cvD(j)
+      qd[p][2] = mul(sg2[1], cvd[0]);  // e = 1: g3 * cvD(jm)
+      qd[p][3] = mul(sg0[1], cvd[1]);  //        g1 * cvD(j)
+    }
+    const int im = wrap(i - 1, Hh);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const T* mb = static_cast<const T*>(bands.ms[b]);
+      const T* mrp = mb + (long long)im * mp;
+      const T* mrc = mb + (long long)i * mp;
+      double llp[2], llc[2];
+      llp[0] = mul((double)__ldg(mrp + jm), 2.0);
+      llp[1] = mul((double)__ldg(mrp + j), 2.0);
+      llc[0] = mul((double)__ldg(mrc + jm), 2.0);
+      llc[1] = mul((double)__ldg(mrc + j), 2.0);
+      T* ob = static_cast<T*>(bands.out[b]);
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        double cva[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          cva[c] = add(add(add(mul(sh2[p], llp[c]), qa0[p][c]), mul(sh0[p], llc[c])), qa1[p][c]);
+        const double o0 = add(add(add(mul(sh2[0], cva[0]), qd[p][0]), mul(sh0[0], cva[1])),
+                              qd[p][1]);
+        const double o1 = add(add(add(mul(sh2[1], cva[0]), qd[p][2]), mul(sh0[1], cva[1])),
+                              qd[p][3]);
+        T* w = ob + (long long)(2 * i + p) * op + 2 * j;
+        if (kVec) {  // one 8/16-byte store per row: the warp's store covers its span densely
+          if constexpr (sizeof(T) == 4)
+            *reinterpret_cast<float2*>(w) = make_float2((float)o0, (float)o1);
+          else
+            *reinterpret_cast<double2*>(w) = make_double2(o0, o1);
+        } else {
+          w[0] = (T)o0;
+          w[1] = (T)o1;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      a[0][c] = a[2][c];
+      a[1][c] = a[3][c];
+      d[0][c] = d[2][c];
+      d[1][c] = d[3][c];
+      lhp[c] = lh[c];
+      hlp[c] = hl[c];
+      hhp[c] = hh[c];
+    }
+  }
+}
+
+template <typename T>
+static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* const* ms, long long mp,
+                                  T* const* out, long long op, int nbands, int h, int w,
+                                  cudaStream_t s) {
+  int rows = kExactRows;
+  if (const char* e = getenv("WF_EXACT_ROWS")) rows = atoi(e) > 0 ? atoi(e) : rows;
+  dim3 grid(((w >> 1) + 127) / 128, ((h >> 1) + rows - 1) / rows);
+  for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
+    const int nb = min(kMaxBandsPerLaunch, nbands - b0);
+    ExactBands eb{};
+    for (int b = 0; b < nb; ++b) {
+      eb.ms[b] = ms[b0 + b];
+      eb.out[b] = out[b0 + b];
+    }
+    bool vec = op % 2 == 0;
+    for (int b = 0; b < nb; ++b)
+      vec = vec && (reinterpret_cast<uintptr_t>(out[b0 + b]) % (2 * sizeof(T))) == 0;
+    switch (nb) {
+#define WF_ED(N)                                                                          \
+  case N:                                                                                 \
+    if (vec)                                                                              \
+      fuse_exact_d4_kernel<T, N, true><<<grid, 128, 0, s>>>(pan, pp, eb, mp, op, h, w, rows); \
+    else                                                                                  \
+      fuse_exact_d4_kernel<T, N, false><<<grid, 128, 0, s>>>(pan, pp, eb, mp, op, h, w, rows); \
+    break;
+      WF_ED(1) WF_ED(2) WF_ED(3) WF_ED(4) WF_ED(5) WF_ED(6) WF_ED(7) WF_ED(8)
+#undef WF_ED
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
                                     long long mp, T* const* out, long long op, int nbands,
@@ -428,6 +734,9 @@ template <typename T>
 cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
                                     long long mp, T* const* out, long long op, int nbands,
                                     int h, int w, double* ws, cudaStream_t s) {
+  if (!getenv("WF_EXACT_TRANSFORMS"))  // one pass, no coefficient image
+    return kind == kHaar ? launch_exact_haar<T>(pan, pp, ms, mp, out, op, nbands, h, w, s)
+                         : launch_exact_d4<T>(pan, pp, ms, mp, out, op, nbands, h, w, s);
   run_dwt2d<T, double>(kind, false, pan, pp, ws, w, h, w, s);
   dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + tr_rows() - 1) / tr_rows());
   for (int b = 0; b < nbands; ++b) {
