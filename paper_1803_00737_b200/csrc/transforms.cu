@@ -552,6 +552,10 @@ static cudaError_t launch_exact_haar(const T* pan, long long pp, const T* const*
 // with every product and sum rounded separately (no FMA), one final cast:
 // bit-identical to the transform path.
 constexpr int kExactRows = 16;
+#ifndef WF_EXACT_AHEAD
+#define WF_EXACT_AHEAD 1
+#endif
+constexpr int kExactAhead = WF_EXACT_AHEAD;  // prefetch distance in row steps
 
 template <typename T, int NB, bool kVec>
 __global__ void __launch_bounds__(128)
@@ -611,7 +615,21 @@ __global__ void __launch_bounds__(128)
       d[1][c] = d[3][c];
     }
   }
+  auto prefetch = [](const void* ptr) { asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr)); };
   for (int i = i0; i < i1; ++i) {
+    // the next step's PAN rows and MS rows into L1 while this step computes
+    // (the loads below are latency-bound at 3 CTAs/SM otherwise)
+    if (i + kExactAhead < i1) {
+#pragma unroll
+      for (int r = 2 + 2 * kExactAhead; r < 4 + 2 * kExactAhead; ++r) {
+        const T* row = pan + (long long)wrap(2 * i + r, H) * pp;
+        prefetch(row + col[0]);
+        prefetch(row + col[5]);
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + kExactAhead) * mp + j);
+    }
     rowpass(wrap(2 * i + 2, H), a[2], d[2]);
     rowpass(wrap(2 * i + 3, H), a[3], d[3]);
     double lh[2], hl[2], hh[2];
