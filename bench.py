@@ -525,6 +525,68 @@ def measure_f64(scene, steps, warmup, dist, world, peak):
     return {"unit": UNIT, "dtype": "f64 in/out, f64 arithmetic", **res}
 
 
+def measure_exact(scene, steps, warmup, dist, world, peak):
+    """The reference-exact mode on the same f32 scene (fuse(..., exact=True),
+    wf_fuse_bands_exact_f32): the reference's own float64 operation sequence
+    (fusion.py:148-150, wavelet.py:73-164), bit-identical outputs, one pass
+    with no coefficient image. Same algorithmic bytes as the fast kernel."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind, _native
+    from paper_1803_00737_b200.scene import scene_bytes
+    from paper_1803_00737_b200.wavelet import KIND_CODE
+
+    lib = _native.load()
+    h, w = scene.shape
+    nbytes = scene_bytes(h, w, len(scene.ms))
+    ws = torch.empty(h * w, dtype=torch.float64, device=scene.pan.device)
+    ms_p = _native.ptr_array([m.data_ptr() for m in scene.ms])
+    out_p = _native.ptr_array([o.data_ptr() for o in scene.out])
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    res = {}
+    for kind in (WaveletKind.HAAR, WaveletKind.DAUB4):
+        code = KIND_CODE[kind]
+
+        def run():
+            _native.check(lib.wf_fuse_bands_exact_f32(code, scene.pan.data_ptr(), w, ms_p, w // 2,
+                                                      out_p, w, len(scene.ms), h, w,
+                                                      ws.data_ptr(), sp))
+
+        for _ in range(warmup):
+            run()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_t = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms_t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_t = float(t.item())
+        per = ms_t / steps
+        achieved = nbytes / (per * 1e-3) / 1e9
+        res[kind.value] = {
+            "value": round(world * h * w / (per * 1e-3) / 1e6, 3),
+            "ms_per_step": round(per, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "kernel": ("fuse_exact_haar_kernel<f32,B=6>" if kind is WaveletKind.HAAR
+                                    else "fuse_exact_d4_kernel<f32,B=6> (float64 transform "
+                                         "order, column-shared)")},
+        }
+    del ws
+    torch.cuda.empty_cache()
+    return {"unit": UNIT, "dtype": "f32 in/out, f64 arithmetic in the reference's order",
+            "parity": "bit-identical to the reference (tests/test_gpu_parity.py)", **res}
+
+
 def measure_u8(scene, steps, warmup, dist, world, dev_index, peak):
     """the same scene in the paper's 8 bpp transfer
     representation (uint8 in, quantised uint8 out, float32 arithmetic). A
@@ -641,6 +703,7 @@ def run_ours(args, rank, world, local_rank):
         }
     u8 = measure_u8(scene, args.steps, args.warmup, dist, world, local_rank, peak)
     f64 = measure_f64(scene, args.steps, args.warmup, dist, world, peak)
+    exact = measure_exact(scene, args.steps, args.warmup, dist, world, peak)
     quality = measure_quality(scene, args.steps, args.warmup, peak)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -700,6 +763,7 @@ def run_ours(args, rank, world, local_rank):
             },
             "u8_8bpp": u8,
             "f64": f64,
+            "exact": exact,
             "quality": quality,
         }
         print(json.dumps(line), flush=True)

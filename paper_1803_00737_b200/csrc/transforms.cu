@@ -557,145 +557,143 @@ constexpr int kExactRows = 16;
 #endif
 constexpr int kExactAhead = WF_EXACT_AHEAD;  // prefetch distance in row steps
 
+// Column sharing: a CTA of 128 threads covers 127 output coefficient columns
+// [127k, 127k + 127); thread t computes column j = 127k - 1 + t, so thread 0's
+// column is the left halo of the CTA (computed, not written). Phase 1 forms
+// everything that depends on one coefficient column -- its forward
+// coefficients, cvD and, per band, cvA -- and publishes it in shared memory;
+// after a barrier, phase 2 combines columns j-1 and j into output columns 2j,
+// 2j+1. Every quantity is computed once (the per-thread form computed column
+// j-1 again), in the same operations and order.
+constexpr int kExCols = 127;
+
 template <typename T, int NB, bool kVec>
 __global__ void __launch_bounds__(128)
     fuse_exact_d4_kernel(const T* __restrict__ pan, long long pp, const ExactBands bands,
                          long long mp, long long op, int H, int W, int rows) {
-  const int j = blockIdx.x * 128 + threadIdx.x;
+  // [buffer][quantity][thread]: quantities cvD[0], cvD[1], cvA[b][0], cvA[b][1]
+  constexpr int NQ = 2 + 2 * NB;
+  __shared__ double xs[2][NQ][128];
+  const int tid = threadIdx.x;
   const int Hh = H >> 1, Wh = W >> 1;
-  if (j >= Wh) return;
+  const int jraw = blockIdx.x * kExCols - 1 + tid;  // -1 .. : thread 0 = halo
+  const int j = wrap(jraw, Wh);
+  const bool emit = tid > 0 && jraw < Wh;
   const int i0 = blockIdx.y * rows;
   const int i1 = min(i0 + rows, Hh);
   const D4 t = d4_taps();
-  const int jm = wrap(j - 1, Wh);
-  // PAN columns 2jm .. 2jm+3 and 2j .. 2j+3 (wrapped): 2j-2 .. 2j+3
-  int col[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) col[k] = wrap(2 * j - 2 + k, W);
-  // row pass of one PAN row at coefficient columns jm (c = 0) and j (c = 1)
-  auto rowpass = [&](int r, double (&a)[2], double (&d)[2]) {
+  const int c0 = 2 * j, c1 = 2 * j + 1, c2 = wrap(2 * j + 2, W), c3 = wrap(2 * j + 3, W);
+  auto rowpass = [&](int r, double& a, double& d) {
     const T* row = pan + (long long)r * pp;
-    double x[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) x[k] = (double)__ldg(row + col[k]);
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      a[c] = fwd_lo(kDaub4, t, x[2 * c], x[2 * c + 1], x[2 * c + 2], x[2 * c + 3]);
-      d[c] = fwd_hi(kDaub4, t, x[2 * c], x[2 * c + 1], x[2 * c + 2], x[2 * c + 3]);
-    }
+    const double x0 = (double)__ldg(row + c0), x1 = (double)__ldg(row + c1);
+    const double x2 = (double)__ldg(row + c2), x3 = (double)__ldg(row + c3);
+    a = fwd_lo(kDaub4, t, x0, x1, x2, x3);
+    d = fwd_hi(kDaub4, t, x0, x1, x2, x3);
   };
-  // column pass of coefficient row i from the row passes of PAN rows 2i..2i+3
-  auto colpass = [&](const double (&a)[4][2], const double (&d)[4][2], double (&lh)[2],
-                     double (&hl)[2], double (&hh)[2]) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      lh[c] = fwd_hi(kDaub4, t, a[0][c], a[1][c], a[2][c], a[3][c]);
-      hl[c] = fwd_lo(kDaub4, t, d[0][c], d[1][c], d[2][c], d[3][c]);
-      hh[c] = fwd_hi(kDaub4, t, d[0][c], d[1][c], d[2][c], d[3][c]);
-    }
-  };
-  // synthesis taps (wavelet.py:96-108): parity p -> (hp2, gp2, hp0, gp0)
   const double sh2[2] = {t.h2, t.h3}, sg2[2] = {t.g2, t.g3};
   const double sh0[2] = {t.h0, t.h1}, sg0[2] = {t.g0, t.g1};
+  auto prefetch = [](const void* ptr) { asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr)); };
 
-  double a[4][2], d[4][2];  // row passes of PAN rows 2i .. 2i+3
-  double lhp[2], hlp[2], hhp[2];  // detail coefficients of row i-1
+  double a[4], d[4];              // row passes of PAN rows 2i .. 2i+3 at column j
+  double lhp, hlp, hhp;           // detail coefficients of row i-1 at column j
   {
     const int im = wrap(i0 - 1, Hh);
     rowpass(2 * im, a[0], d[0]);
     rowpass(2 * im + 1, a[1], d[1]);
     rowpass(2 * i0, a[2], d[2]);
     rowpass(2 * i0 + 1, a[3], d[3]);
-    colpass(a, d, lhp, hlp, hhp);
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      a[0][c] = a[2][c];
-      a[1][c] = a[3][c];
-      d[0][c] = d[2][c];
-      d[1][c] = d[3][c];
-    }
+    lhp = fwd_hi(kDaub4, t, a[0], a[1], a[2], a[3]);
+    hlp = fwd_lo(kDaub4, t, d[0], d[1], d[2], d[3]);
+    hhp = fwd_hi(kDaub4, t, d[0], d[1], d[2], d[3]);
+    a[0] = a[2];
+    a[1] = a[3];
+    d[0] = d[2];
+    d[1] = d[3];
   }
-  auto prefetch = [](const void* ptr) { asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr)); };
-  for (int i = i0; i < i1; ++i) {
-    // the next step's PAN rows and MS rows into L1 while this step computes
-    // (the loads below are latency-bound at 3 CTAs/SM otherwise)
-    if (i + kExactAhead < i1) {
+  int buf = 0;
+  for (int i = i0; i < i1; ++i, buf ^= 1) {
+    if (i + 1 < i1) {  // next step's PAN and MS lines into L1
 #pragma unroll
-      for (int r = 2 + 2 * kExactAhead; r < 4 + 2 * kExactAhead; ++r) {
+      for (int r = 4; r < 6; ++r) {
         const T* row = pan + (long long)wrap(2 * i + r, H) * pp;
-        prefetch(row + col[0]);
-        prefetch(row + col[5]);
+        prefetch(row + c0);
+        prefetch(row + c3);
       }
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + kExactAhead) * mp + j);
+        prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + 1) * mp + j);
     }
+    // ---- phase 1: column j ----
     rowpass(wrap(2 * i + 2, H), a[2], d[2]);
     rowpass(wrap(2 * i + 3, H), a[3], d[3]);
-    double lh[2], hl[2], hh[2];
-    colpass(a, d, lh, hl, hh);
-    // PAN-only parts of the inverse
-    double qa0[2][2], qa1[2][2], qd[2][4];
+    const double lh = fwd_hi(kDaub4, t, a[0], a[1], a[2], a[3]);
+    const double hl = fwd_lo(kDaub4, t, d[0], d[1], d[2], d[3]);
+    const double hh = fwd_hi(kDaub4, t, d[0], d[1], d[2], d[3]);
+    double cvd[2], qa0[2], qa1[2];
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-      double cvd[2];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        cvd[c] = add(add(add(mul(sh2[p], hlp[c]), mul(sg2[p], hhp[c])), mul(sh0[p], hl[c])),
-                     mul(sg0[p], hh[c]));
-        qa0[p][c] = mul(sg2[p], lhp[c]);
-        qa1[p][c] = mul(sg0[p], lh[c]);
-      }
-      // output column parity e: (he2, ge2, he0, ge0) applied to (cvA(jm), cvD(jm), cvA(j), cvD(j))
-      qd[p][0] = mul(sg2[0], cvd[0]);  // e = 0: g2 * cvD(jm)
-      qd[p][1] = mul(sg0[0], cvd[1]);  //        g0 * cvD(j)
-      qd[p][2] = mul(sg2[1], cvd[0]);  // e = 1: g3 * cvD(jm)
-      qd[p][3] = mul(sg0[1], cvd[1]);  //        g1 * cvD(j)
+      cvd[p] = add(add(add(mul(sh2[p], hlp), mul(sg2[p], hhp)), mul(sh0[p], hl)), mul(sg0[p], hh));
+      qa0[p] = mul(sg2[p], lhp);
+      qa1[p] = mul(sg0[p], lh);
+      xs[buf][p][tid] = cvd[p];
     }
     const int im = wrap(i - 1, Hh);
+    double cva[NB][2];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const T* mb = static_cast<const T*>(bands.ms[b]);
-      const T* mrp = mb + (long long)im * mp;
-      const T* mrc = mb + (long long)i * mp;
-      double llp[2], llc[2];
-      llp[0] = mul((double)__ldg(mrp + jm), 2.0);
-      llp[1] = mul((double)__ldg(mrp + j), 2.0);
-      llc[0] = mul((double)__ldg(mrc + jm), 2.0);
-      llc[1] = mul((double)__ldg(mrc + j), 2.0);
-      T* ob = static_cast<T*>(bands.out[b]);
+      const double llp = mul((double)__ldg(mb + (long long)im * mp + j), 2.0);
+      const double llc = mul((double)__ldg(mb + (long long)i * mp + j), 2.0);
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
-        double cva[2];
+        cva[b][p] = add(add(add(mul(sh2[p], llp), qa0[p]), mul(sh0[p], llc)), qa1[p]);
+        xs[buf][2 + 2 * b + p][tid] = cva[b][p];
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: output columns 2j, 2j+1 from columns j-1 and j ----
+    if (emit) {
+      double qd[2][4];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          cva[c] = add(add(add(mul(sh2[p], llp[c]), qa0[p][c]), mul(sh0[p], llc[c])), qa1[p][c]);
-        const double o0 = add(add(add(mul(sh2[0], cva[0]), qd[p][0]), mul(sh0[0], cva[1])),
-                              qd[p][1]);
-        const double o1 = add(add(add(mul(sh2[1], cva[0]), qd[p][2]), mul(sh0[1], cva[1])),
-                              qd[p][3]);
-        T* w = ob + (long long)(2 * i + p) * op + 2 * j;
-        if (kVec) {  // one 8/16-byte store per row: the warp's store covers its span densely
-          if constexpr (sizeof(T) == 4)
-            *reinterpret_cast<float2*>(w) = make_float2((float)o0, (float)o1);
-          else
-            *reinterpret_cast<double2*>(w) = make_double2(o0, o1);
-        } else {
-          w[0] = (T)o0;
-          w[1] = (T)o1;
+      for (int p = 0; p < 2; ++p) {
+        const double cvdm = xs[buf][p][tid - 1];
+        qd[p][0] = mul(sg2[0], cvdm);
+        qd[p][1] = mul(sg0[0], cvd[p]);
+        qd[p][2] = mul(sg2[1], cvdm);
+        qd[p][3] = mul(sg0[1], cvd[p]);
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        T* ob = static_cast<T*>(bands.out[b]);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const double cvam = xs[buf][2 + 2 * b + p][tid - 1];
+          const double o0 = add(add(add(mul(sh2[0], cvam), qd[p][0]), mul(sh0[0], cva[b][p])),
+                                qd[p][1]);
+          const double o1 = add(add(add(mul(sh2[1], cvam), qd[p][2]), mul(sh0[1], cva[b][p])),
+                                qd[p][3]);
+          T* w = ob + (long long)(2 * i + p) * op + 2 * j;
+          if (kVec) {
+            if constexpr (sizeof(T) == 4)
+              *reinterpret_cast<float2*>(w) = make_float2((float)o0, (float)o1);
+            else
+              *reinterpret_cast<double2*>(w) = make_double2(o0, o1);
+          } else {
+            w[0] = (T)o0;
+            w[1] = (T)o1;
+          }
         }
       }
     }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      a[0][c] = a[2][c];
-      a[1][c] = a[3][c];
-      d[0][c] = d[2][c];
-      d[1][c] = d[3][c];
-      lhp[c] = lh[c];
-      hlp[c] = hl[c];
-      hhp[c] = hh[c];
-    }
+    // (xs is double-buffered: the next step writes the other buffer, and the
+    // barrier of that step orders this step's reads before it is reused)
+    a[0] = a[2];
+    a[1] = a[3];
+    d[0] = d[2];
+    d[1] = d[3];
+    lhp = lh;
+    hlp = hl;
+    hhp = hh;
   }
 }
 
@@ -705,7 +703,7 @@ static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* const* m
                                   cudaStream_t s) {
   int rows = kExactRows;
   if (const char* e = getenv("WF_EXACT_ROWS")) rows = atoi(e) > 0 ? atoi(e) : rows;
-  dim3 grid(((w >> 1) + 127) / 128, ((h >> 1) + rows - 1) / rows);
+  dim3 grid(((w >> 1) + kExCols - 1) / kExCols, ((h >> 1) + rows - 1) / rows);
   for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
     const int nb = min(kMaxBandsPerLaunch, nbands - b0);
     ExactBands eb{};
