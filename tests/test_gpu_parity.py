@@ -435,3 +435,23 @@ def test_exact_mode_multi_cta_vs_oracle(kname, dt):
         assert np.array_equal(o, r)
     one = wf.fuse_dwt(pan, bands[1], KINDS[kname], exact=True)
     assert np.array_equal(one, got[1])
+
+
+@pytest.mark.parametrize("kname,shape,nb", [("haar", (2, 2), 1), ("haar", (6, 10), 2),
+                                            ("daub4", (4, 4), 1), ("daub4", (6, 10), 3),
+                                            ("daub4", (8, 260), 9), ("haar", (10, 518), 9)])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_exact_mode_edge_shapes(kname, shape, nb, dt):
+    """The one-pass exact kernels at the smallest legal planes, widths that
+    are 2 mod 4 (the scalar Haar path), a single CTA column band narrower
+    than its halo, and more than 8 bands (several launches): bit-identical to
+    the pinned float64 oracle."""
+    rng = np.random.default_rng(23)
+    h, w = shape
+    pan = rng.uniform(0, 255, (h, w)).astype(dt)
+    bands = [rng.uniform(0, 255, (h // 2, w // 2)).astype(dt) for _ in range(nb)]
+    got = wf.fuse(pan, bands, wf.DwtReplace(KINDS[kname]), exact=True)
+    ref = O.fuse(pan, bands, kname)
+    for o, r in zip(got, ref):
+        assert o.dtype == r.dtype
+        assert np.array_equal(o, r)
