@@ -577,6 +577,9 @@ def measure_exact(scene, steps, warmup, dist, world, peak):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_launch": nbytes,
+                         "traffic": ncu_traffic("fuse_exact_haar_kernel_float__6__1"
+                                                if kind is WaveletKind.HAAR
+                                                else "fuse_exact_d4_kernel_float__6__1"),
                          "kernel": ("fuse_exact_haar_kernel<f32,B=6>" if kind is WaveletKind.HAAR
                                     else "fuse_exact_d4_kernel<f32,B=6> (float64 transform "
                                          "order, column-shared)")},
