@@ -113,9 +113,9 @@ int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const doub
 /* Reference-exact fuse_dwt (fusion.py:148-150 step by step): float64
  * forward transform in the reference's operation order, LL <- band * gain,
  * float64 inverse, one final cast -- bit-identical to the reference for f32
- * and f64 callers. Two launches (forward; inverse forming LL = band * gain
- * as it reads) and an h*w float64 coefficient workspace (8*h*w bytes,
- * caller-owned). */
+ * and f64 callers. One pass (see wf_fuse_bands_exact_*); the h*w float64
+ * workspace (8*h*w bytes, caller-owned) is only used by the
+ * WF_EXACT_TRANSFORMS=1 sequence. */
 int wf_fuse_dwt_exact_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,
                           int64_t ms_pitch, float* out, int64_t out_pitch, int h, int w,
                           void* workspace, void* stream);
@@ -124,12 +124,12 @@ int wf_fuse_dwt_exact_f64(int kind, const double* pan, int64_t pan_pitch, const 
                           void* workspace, void* stream);
 
 /* fuse(pan, bands, DwtReplace(kind)) in the reference-exact sequence
- * (fusion.py:182 calling fusion.py:148-150 per band), with the PAN's float64
- * forward transform computed ONCE for all bands: the detail quadrants of the
- * workspace are never written after the forward pass, and LL is fully
- * overwritten per band, so each band's inverse sees exactly the coefficients
- * the reference's per-band fuse_dwt builds. Bit-identical to calling
- * wf_fuse_dwt_exact_* per band. Any band count (no kMaxBands limit). */
+ * (fusion.py:182 calling fusion.py:148-150 per band), bit-identical to
+ * calling wf_fuse_dwt_exact_* per band. One pass with no coefficient image:
+ * the reference's float64 forward operations on the PAN (once for all
+ * bands), LL = band * gain, its float64 inverse, one cast. `workspace`
+ * (8*h*w bytes, caller-owned) is only used when WF_EXACT_TRANSFORMS=1
+ * selects the transform-kernel sequence. Any band count. */
 int wf_fuse_bands_exact_f32(int kind, const float* pan, int64_t pan_pitch,
                             const float* const* ms, int64_t ms_pitch, float* const* out,
                             int64_t out_pitch, int nbands, int h, int w, void* workspace,
