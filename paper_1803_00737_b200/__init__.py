@@ -29,6 +29,7 @@ from .errors import (
 from .fusion import (
     DwtReplace,
     FusionMethod,
+    set_exact_default,
     fuse,
     fuse_dwt,
     fuse_quantized,
@@ -102,6 +103,7 @@ __all__ = [
     "q_index",
     "qnr",
     "qnr_async",
+    "set_exact_default",
     "PendingReport",
     "quantize",
     "read_pnm",

@@ -179,7 +179,7 @@ def _raster_from_planes(planes: list[torch.Tensor], h: int, w: int) -> np.ndarra
 
 
 def fuse_pnm(pan: bytes, ms: list[bytes], method: FusionMethod, grid: tuple[int, int] = (1, 1),
-             *, exact: bool = False) -> list[bytes]:
+             *, exact: bool | None = None) -> list[bytes]:
     """The data path of the reference's `wavefuse fuse` (cli.py:147-165) for
     DwtReplace methods, in memory: PGM PAN + band files (one PPM = 3 bands,
     else one PGM per band) -> the PNM files it would write (cli.py:135-144):

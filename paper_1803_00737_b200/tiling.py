@@ -13,6 +13,8 @@ strips.py, which exchanges halos instead.)
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,6 +25,7 @@ from .errors import BandCountMismatch, DimensionMismatch, NotDivisible, OddTile,
 from .fusion import (
     DwtReplace,
     FusionMethod,
+    _exact,
     _quantize_dev,
     _u8_device,
     _u8_to_f32_dev,
@@ -121,16 +124,19 @@ def _window_fuse(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
                  out: list[torch.Tensor], grid: TileGrid, exact: bool = False) -> None:
     """One fused launch per tile on strided windows of the device scene; each
     tile wraps periodically within itself. exact=True runs the reference's
-    float64 operation order per tile and band (wf_fuse_dwt_exact_*)."""
+    float64 operation order per tile for all bands (wf_fuse_bands_exact_*)."""
     lib = _native.load()
     esz = pan.element_size()
     tw, th = grid.pan_tile_w, grid.pan_tile_h
     pp, mp, op = pan.stride(0), ms[0].stride(0), out[0].stride(0)
     s = _device.stream_ptr()
     code = KIND_CODE[kind]
-    if exact:
-        fn = lib.wf_fuse_dwt_exact_f32 if pan.dtype == torch.float32 else lib.wf_fuse_dwt_exact_f64
-        ws = torch.empty((th, tw), dtype=torch.float64, device=pan.device)
+    if exact:  # one launch per tile for all bands (the one-pass exact kernels)
+        fn = (lib.wf_fuse_bands_exact_f32 if pan.dtype == torch.float32
+              else lib.wf_fuse_bands_exact_f64)
+        ws = torch.empty(1, dtype=torch.float64, device=pan.device)  # unused by the one-pass path
+        if os.environ.get("WF_EXACT_TRANSFORMS"):
+            ws = torch.empty((th, tw), dtype=torch.float64, device=pan.device)
     else:
         fn = {torch.float32: lib.wf_fuse_bands_f32, torch.float64: lib.wf_fuse_bands_f64,
               torch.uint8: lib.wf_fuse_bands_u8}[pan.dtype]
@@ -141,8 +147,8 @@ def _window_fuse(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
             ms_a = [m.data_ptr() + ((r0 // 2) * mp + c0 // 2) * esz for m in ms]
             out_a = [o.data_ptr() + (r0 * op + c0) * esz for o in out]
             if exact:
-                for m_p, o_p in zip(ms_a, out_a):
-                    _native.check(fn(code, pan_p, pp, m_p, mp, o_p, op, th, tw, ws.data_ptr(), s))
+                _native.check(fn(code, pan_p, pp, _native.ptr_array(ms_a), mp,
+                                 _native.ptr_array(out_a), op, len(ms), th, tw, ws.data_ptr(), s))
             else:
                 _native.check(fn(code, pan_p, pp, _native.ptr_array(ms_a), mp,
                                  _native.ptr_array(out_a), op, len(ms), th, tw, s))
@@ -155,7 +161,7 @@ def _u8_windows_ok(grid: TileGrid, kind: WaveletKind) -> bool:
 
 
 def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
-               transfer_8bpp: bool = False, *, exact: bool = False):
+               transfer_8bpp: bool = False, *, exact: bool | None = None):
     """tiling.py:213-273 for DwtReplace. `workers` is accepted for signature
     compatibility (the GPU fuses tiles, not a thread pool). Plain mode
     resamples bands globally, then fuses every tile with per-tile wrap (float
@@ -164,6 +170,7 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
     reproduces the distributed pipeline: inputs quantised to uint8
     (wire_planes, tiling.py:192-210), each tile fused in float32 and quantised
     (tiling.py:163-172, 268-269)."""
+    exact = _exact(exact)
     if workers < 1:
         raise ValueError(f"workers {workers} must be >= 1")
     is_t = isinstance(pan, torch.Tensor)

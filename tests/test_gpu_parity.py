@@ -455,3 +455,22 @@ def test_exact_mode_edge_shapes(kname, shape, nb, dt):
     for o, r in zip(got, ref):
         assert o.dtype == r.dtype
         assert np.array_equal(o, r)
+
+
+def test_exact_default_switch(golden_fusion):
+    """set_exact_default(True) makes the reference's own signatures
+    (fuse_dwt(pan, band, kind), fuse(pan, bands, method)) return the
+    reference's bits -- the switch a drop-in binding uses, since those
+    signatures have no `exact` keyword."""
+    g = golden_fusion
+    name = next(n for n in _cases(g) if f"{n}/daub4/out0" in g)
+    pan, bands = g[f"{name}/pan"], _bands(g, name)
+    try:
+        wf.set_exact_default(True)
+        got = wf.fuse(pan, bands, wf.DwtReplace(wf.WaveletKind.DAUB4))
+        one = wf.fuse_dwt(pan, bands[0], wf.WaveletKind.DAUB4)
+    finally:
+        wf.set_exact_default(False)
+    for b, o in enumerate(got):
+        assert np.array_equal(o, g[f"{name}/daub4/out{b}"])
+    assert np.array_equal(one, g[f"{name}/daub4/out0"])
