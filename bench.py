@@ -313,7 +313,7 @@ def measure_device(scene, kind, steps, warmup, dist, world, dev_index):
     return ms, launches, clk.summary()
 
 
-def measure_e2e(scene, kind, steps, dist, pan_d=None, ms_d=None, ref_out=None):
+def measure_e2e(scene, kind, steps, dist, pan_d=None, ms_d=None, ref_out=None, exact=False):
     """End to end through the public host-buffer C ABI (wf_fuse_host_f32, or
     wf_fuse_host_u8 for uint8 planes): every step copies the scene's inputs
     from pinned host memory, fuses, and reads every fused band back into
@@ -333,6 +333,7 @@ def measure_e2e(scene, kind, steps, dist, pan_d=None, ms_d=None, ref_out=None):
     ms_h = [m.cpu().pin_memory() for m in ms_d]
     out_h = [torch.empty(pan_d.shape, dtype=pan_d.dtype).pin_memory() for _ in ms_d]
     ctx = lib.wf_ctx_create(torch.cuda.current_device(), 1024)
+    _native.check(lib.wf_ctx_set_exact(ctx, 1 if exact else 0))
     ms_p = _native.ptr_array([m.data_ptr() for m in ms_h])
     out_p = _native.ptr_array([o.data_ptr() for o in out_h])
     h, w = scene.shape
@@ -571,9 +572,17 @@ def measure_exact(scene, steps, warmup, dist, world, peak):
             ms_t = float(t.item())
         per = ms_t / steps
         achieved = nbytes / (per * 1e-3) / 1e9
+        sec, h2d, d2h, ok = measure_e2e(scene, kind, max(2, min(steps, 5)), dist,
+                                        ref_out=scene.out, exact=True)
+        e2e_steps = max(2, min(steps, 5))
         res[kind.value] = {
             "value": round(world * h * w / (per * 1e-3) / 1e6, 3),
             "ms_per_step": round(per, 4),
+            "e2e": {"value": round(world * h * w * e2e_steps / sec / 1e6, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "wf_fuse_host_f32 with wf_ctx_set_exact (pinned host buffers, "
+                           "strips of 1024 rows with halo rows)",
+                    "matches_device_result": ok},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_launch": nbytes,

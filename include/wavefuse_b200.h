@@ -143,6 +143,11 @@ int wf_fuse_bands_exact_f64(int kind, const double* pan, int64_t pan_pitch,
 typedef struct wf_ctx wf_ctx;
 /* strip_rows: PAN rows per pipeline stage (even; 0 = default 512). */
 wf_ctx* wf_ctx_create(int device, int strip_rows);
+/* exact != 0: the context's strips run the reference-exact one-pass kernels
+ * (the float64 sequence of fusion.py:148-150 with the neighbouring strips'
+ * halo rows) -- bit-identical host-buffer fusion at PCIe speed. u8 calls are
+ * unaffected. */
+int wf_ctx_set_exact(wf_ctx* ctx, int exact);
 void wf_ctx_destroy(wf_ctx* ctx);
 int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const* ms,
                      float* const* out, int nbands, int h, int w);

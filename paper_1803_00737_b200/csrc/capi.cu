@@ -72,7 +72,7 @@ template <typename T>
 int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, const T* pan_bot,
                 int64_t halo_pitch, const T* const* ms, const T* const* ms_top, int64_t ms_pitch,
                 T* const* out, int64_t out_pitch, int nbands, int rows, int w, bool strip,
-                cudaStream_t s) {
+                cudaStream_t s, bool exact = false) {
   if (int e = check_kind(kind)) return e;
   if (nbands < 1) return fail(WF_ERR_BAND_COUNT, "need at least one band");
   if (!pan || !ms || !out) return fail(WF_ERR_VALUE, "null pointer argument");
@@ -88,6 +88,18 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
     return fail(WF_ERR_VALUE, "pitch smaller than row length");
   if (kind == WF_DAUB4 && strip && (!pan_top || !pan_bot || !ms_top))
     return fail(WF_ERR_VALUE, "D4 strip needs halo pointers");
+  for (int b = 0; b < nbands; ++b)
+    if (!ms[b] || !out[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
+  if constexpr (sizeof(T) != 1) {
+    if (exact) {  // the reference's float64 sequence, one pass (transforms.cu)
+      cudaError_t e = wf::launch_fuse_exact_strip<T>(
+          kind, pan, pan_pitch, strip ? pan_top : nullptr, strip ? pan_bot : nullptr, halo_pitch,
+          ms, strip ? ms_top : nullptr, ms_pitch, out, out_pitch, nbands, rows, w, s);
+      if (e != cudaSuccess) return cuda_status(e, "exact fuse launch");
+      g_launches += (nbands + wf::kMaxBandsPerLaunch - 1) / wf::kMaxBandsPerLaunch;
+      return WF_OK;
+    }
+  }
 
   const int vw = 16 / (int)sizeof(T);  // elements per 16 B
   bool vec = al16(pan) && pan_pitch % vw == 0 && out_pitch % vw == 0 && ms_pitch % 2 == 0;
@@ -278,6 +290,7 @@ struct Slot {
 struct wf_ctx {
   int device = 0;
   int strip_rows = 512;
+  int exact = 0;  // wf_ctx_set_exact: strips run the reference-exact kernels
   Slot slot[kSlots];
   std::unique_ptr<CopyPool> pool;  // created on first pageable call
 };
@@ -440,7 +453,7 @@ int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const*
     if (e != cudaSuccess) return cuda_status(e, "H2D");
     if (int rc = fuse_common<T>(kind, dbase + L.pan, w, dbase + L.top, dbase + L.bot, w,
                                 dms.data(), dmst.data(), wh, dout.data(), w, nbands, rows, w,
-                                true, st))
+                                true, st, ctx->exact != 0))
       return rc;
     for (int b = 0; b < nbands && e == cudaSuccess; ++b) {
       T* dst = pinned ? out[b] + (size_t)r0 * w : hbase + L.out[b];
@@ -508,6 +521,12 @@ int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const doub
   return fuse_common<double>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
                              ms_pitch, out, out_pitch, nbands, rows, w, true,
                              (cudaStream_t)stream);
+}
+
+int wf_ctx_set_exact(wf_ctx* ctx, int exact) {
+  if (!ctx) return fail(WF_ERR_VALUE, "null context");
+  ctx->exact = exact ? 1 : 0;
+  return WF_OK;
 }
 
 wf_ctx* wf_ctx_create(int device, int strip_rows) {

@@ -421,6 +421,15 @@ cudaError_t launch_synth(float* out, long long pitch, int rows, int cols, unsign
 struct ExactBands {
   const void* ms[kMaxBandsPerLaunch];
   void* out[kMaxBandsPerLaunch];
+  // D4 halos (the RowSrc convention of fuse.cu): PAN logical rows -2, -1 at
+  // pan_top and rows H, H+1 at pan_bot (halo_pitch apart), MS row -1 of each
+  // band at ms_top. A whole plane aliases them to its own wrapped rows
+  // (wavelet.py:83-84); a row strip (host pipeline, strips.py) passes its
+  // neighbours' rows.
+  const void* pan_top;
+  const void* pan_bot;
+  long long halo_pitch;
+  const void* ms_top[kMaxBandsPerLaunch];
 };
 
 template <typename T, int NB, bool kVec>
@@ -583,8 +592,14 @@ __global__ void __launch_bounds__(128)
   const int i1 = min(i0 + rows, Hh);
   const D4 t = d4_taps();
   const int c0 = 2 * j, c1 = 2 * j + 1, c2 = wrap(2 * j + 2, W), c3 = wrap(2 * j + 3, W);
+  // PAN logical row r (-2 .. H+1) through the halo sources
+  auto pan_row = [&](int r) -> const T* {
+    if (r < 0) return static_cast<const T*>(bands.pan_top) + (long long)(r + 2) * bands.halo_pitch;
+    if (r >= H) return static_cast<const T*>(bands.pan_bot) + (long long)(r - H) * bands.halo_pitch;
+    return pan + (long long)r * pp;
+  };
   auto rowpass = [&](int r, double& a, double& d) {
-    const T* row = pan + (long long)r * pp;
+    const T* row = pan_row(r);
     const double x0 = (double)__ldg(row + c0), x1 = (double)__ldg(row + c1);
     const double x2 = (double)__ldg(row + c2), x3 = (double)__ldg(row + c3);
     a = fwd_lo(kDaub4, t, x0, x1, x2, x3);
@@ -597,9 +612,8 @@ __global__ void __launch_bounds__(128)
   double a[4], d[4];              // row passes of PAN rows 2i .. 2i+3 at column j
   double lhp, hlp, hhp;           // detail coefficients of row i-1 at column j
   {
-    const int im = wrap(i0 - 1, Hh);
-    rowpass(2 * im, a[0], d[0]);
-    rowpass(2 * im + 1, a[1], d[1]);
+    rowpass(2 * i0 - 2, a[0], d[0]);  // coefficient row i0 - 1 (the top halo when i0 = 0)
+    rowpass(2 * i0 - 1, a[1], d[1]);
     rowpass(2 * i0, a[2], d[2]);
     rowpass(2 * i0 + 1, a[3], d[3]);
     lhp = fwd_hi(kDaub4, t, a[0], a[1], a[2], a[3]);
@@ -615,7 +629,7 @@ __global__ void __launch_bounds__(128)
     if (i + 1 < i1) {  // next step's PAN and MS lines into L1
 #pragma unroll
       for (int r = 4; r < 6; ++r) {
-        const T* row = pan + (long long)wrap(2 * i + r, H) * pp;
+        const T* row = pan_row(2 * i + r);
         prefetch(row + c0);
         prefetch(row + c3);
       }
@@ -624,8 +638,8 @@ __global__ void __launch_bounds__(128)
         prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + 1) * mp + j);
     }
     // ---- phase 1: column j ----
-    rowpass(wrap(2 * i + 2, H), a[2], d[2]);
-    rowpass(wrap(2 * i + 3, H), a[3], d[3]);
+    rowpass(2 * i + 2, a[2], d[2]);
+    rowpass(2 * i + 3, a[3], d[3]);
     const double lh = fwd_hi(kDaub4, t, a[0], a[1], a[2], a[3]);
     const double hl = fwd_lo(kDaub4, t, d[0], d[1], d[2], d[3]);
     const double hh = fwd_hi(kDaub4, t, d[0], d[1], d[2], d[3]);
@@ -637,12 +651,12 @@ __global__ void __launch_bounds__(128)
       qa1[p] = mul(sg0[p], lh);
       xs[buf][p][tid] = cvd[p];
     }
-    const int im = wrap(i - 1, Hh);
     double cva[NB][2];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const T* mb = static_cast<const T*>(bands.ms[b]);
-      const double llp = mul((double)__ldg(mb + (long long)im * mp + j), 2.0);
+      const T* mprev = i > 0 ? mb + (long long)(i - 1) * mp : static_cast<const T*>(bands.ms_top[b]);
+      const double llp = mul((double)__ldg(mprev + j), 2.0);
       const double llc = mul((double)__ldg(mb + (long long)i * mp + j), 2.0);
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -698,18 +712,23 @@ __global__ void __launch_bounds__(128)
 }
 
 template <typename T>
-static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* const* ms, long long mp,
-                                  T* const* out, long long op, int nbands, int h, int w,
-                                  cudaStream_t s) {
+static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* pan_top, const T* pan_bot,
+                                  long long hp, const T* const* ms, const T* const* ms_top,
+                                  long long mp, T* const* out, long long op, int nbands, int h,
+                                  int w, cudaStream_t s) {
   int rows = kExactRows;
   if (const char* e = getenv("WF_EXACT_ROWS")) rows = atoi(e) > 0 ? atoi(e) : rows;
   dim3 grid(((w >> 1) + kExCols - 1) / kExCols, ((h >> 1) + rows - 1) / rows);
   for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
     const int nb = min(kMaxBandsPerLaunch, nbands - b0);
     ExactBands eb{};
+    eb.pan_top = pan_top;
+    eb.pan_bot = pan_bot;
+    eb.halo_pitch = hp;
     for (int b = 0; b < nb; ++b) {
       eb.ms[b] = ms[b0 + b];
       eb.out[b] = out[b0 + b];
+      eb.ms_top[b] = ms_top[b0 + b];
     }
     bool vec = op % 2 == 0;
     for (int b = 0; b < nb; ++b)
@@ -729,6 +748,38 @@ static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* const* m
   }
   return cudaGetLastError();
 }
+
+// Row strips (host pipeline, strips.py): the one-pass exact kernels with the
+// neighbours' halo rows (D4; Haar needs none). pan_top == nullptr: a whole
+// plane, whose halos are its own wrapped rows.
+template <typename T>
+cudaError_t launch_fuse_exact_strip(int kind, const T* pan, long long pp, const T* pan_top,
+                                    const T* pan_bot, long long hp, const T* const* ms,
+                                    const T* const* ms_top, long long mp, T* const* out,
+                                    long long op, int nbands, int rows, int w, cudaStream_t s) {
+  if (kind == kHaar) return launch_exact_haar<T>(pan, pp, ms, mp, out, op, nbands, rows, w, s);
+  if (pan_top) return launch_exact_d4<T>(pan, pp, pan_top, pan_bot, hp, ms, ms_top, mp, out, op,
+                                         nbands, rows, w, s);
+  for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
+    const int nb = min(kMaxBandsPerLaunch, nbands - b0);
+    const T* mst[kMaxBandsPerLaunch];
+    for (int b = 0; b < nb; ++b) mst[b] = ms[b0 + b] + (long long)(rows / 2 - 1) * mp;
+    const cudaError_t e = launch_exact_d4<T>(pan, pp, pan + (long long)(rows - 2) * pp, pan, pp,
+                                             ms + b0, mst, mp, out + b0, op, nb, rows, w, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+template cudaError_t launch_fuse_exact_strip<float>(int, const float*, long long, const float*,
+                                                    const float*, long long, const float* const*,
+                                                    const float* const*, long long,
+                                                    float* const*, long long, int, int, int,
+                                                    cudaStream_t);
+template cudaError_t launch_fuse_exact_strip<double>(int, const double*, long long, const double*,
+                                                     const double*, long long,
+                                                     const double* const*, const double* const*,
+                                                     long long, double* const*, long long, int,
+                                                     int, int, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
@@ -751,8 +802,8 @@ cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const 
                                     long long mp, T* const* out, long long op, int nbands,
                                     int h, int w, double* ws, cudaStream_t s) {
   if (!getenv("WF_EXACT_TRANSFORMS"))  // one pass, no coefficient image
-    return kind == kHaar ? launch_exact_haar<T>(pan, pp, ms, mp, out, op, nbands, h, w, s)
-                         : launch_exact_d4<T>(pan, pp, ms, mp, out, op, nbands, h, w, s);
+    return launch_fuse_exact_strip<T>(kind, pan, pp, nullptr, nullptr, 0, ms, nullptr, mp, out,
+                                      op, nbands, h, w, s);
   run_dwt2d<T, double>(kind, false, pan, pp, ws, w, h, w, s);
   dim3 grid(((w >> 1) + kTrThreads - 1) / kTrThreads, ((h >> 1) + tr_rows() - 1) / tr_rows());
   for (int b = 0; b < nbands; ++b) {

@@ -88,6 +88,11 @@ template <typename T>
 cudaError_t launch_fuse_exact(int kind, const T* pan, long long pp, const T* ms, long long mp,
                               T* out, long long op, int h, int w, double* ws, cudaStream_t s);
 template <typename T>
+cudaError_t launch_fuse_exact_strip(int kind, const T* pan, long long pp, const T* pan_top,
+                                    const T* pan_bot, long long hp, const T* const* ms,
+                                    const T* const* ms_top, long long mp, T* const* out,
+                                    long long op, int nbands, int rows, int w, cudaStream_t s);
+template <typename T>
 cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
                                     long long mp, T* const* out, long long op, int nbands,
                                     int h, int w, double* ws, cudaStream_t s);

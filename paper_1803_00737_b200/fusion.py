@@ -135,9 +135,10 @@ def _fuse_device(pan_t: torch.Tensor, bands_t: list[torch.Tensor], kind: Wavelet
 
 
 def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
-               out_dt) -> list[np.ndarray]:
+               out_dt, exact: bool = False) -> list[np.ndarray]:
     """All bands through the library's host-buffer pipeline (H2D / fuse / D2H
-    overlapped per row strip)."""
+    overlapped per row strip). exact=True: the strips run the reference-exact
+    one-pass kernels with their neighbours' halo rows (wf_ctx_set_exact)."""
     h, w = pan.shape
     pan_c = np.ascontiguousarray(pan, dtype=out_dt)
     band_c = [np.ascontiguousarray(b, dtype=out_dt) for b in bands]
@@ -147,6 +148,7 @@ def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
     ms_ptrs = _native.ptr_array([b.ctypes.data for b in band_c])
     out_ptrs = _native.ptr_array([o.ctypes.data for o in outs])
     with _device.host_ctx() as ctx:
+        _native.check(lib.wf_ctx_set_exact(ctx, 1 if exact else 0))
         _native.check(fn(ctx, KIND_CODE[kind], pan_c.ctypes.data, ms_ptrs, out_ptrs,
                          len(bands), h, w))
     return outs
@@ -190,10 +192,11 @@ def fuse_dwt(pan, ms_band, kind: WaveletKind, *, exact: bool | None = None):
     h, w = _validate_pair(_shape(pan), _shape(ms_band))
     _check_min(h, w, kind)
     out_dt = _device.np_out_dtype(pan)
+    if exact and _is_tensor(pan):
+        return _fuse_exact_device(_device.to_device(pan, out_dt),
+                                  [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
     if exact:
-        o = _fuse_exact_device(_device.to_device(pan, out_dt),
-                               [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
-        return o if _is_tensor(pan) else o.cpu().numpy()
+        return _fuse_host(pan, [np.asarray(ms_band)], kind, out_dt, exact=True)[0]
     if _is_tensor(pan):
         pan_t = _device.to_device(pan, out_dt)
         return _fuse_device(pan_t, [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
@@ -233,11 +236,14 @@ def fuse(pan, ms, method: FusionMethod, *, exact: bool | None = None):
         _validate_pair(shape, _shape(b))
     _check_min(h, w, method.kind)
     out_dt = _device.np_out_dtype(pan)
-    if exact:
+    if exact and (_is_tensor(pan) or any(_is_tensor(b) for b in resampled)):
         outs = _fuse_exact_device(_device.to_device(pan, out_dt),
                                   [_device.to_device(b, out_dt) for b in resampled],
                                   method.kind, out_dt)
         return outs if _is_tensor(pan) else [o.cpu().numpy() for o in outs]
+    if exact:  # host buffers: the strip pipeline with the exact kernels
+        return _fuse_host(pan, [np.asarray(b) for b in resampled], method.kind, out_dt,
+                          exact=True)
     if _is_tensor(pan) or any(_is_tensor(b) for b in resampled):
         pan_t = _device.to_device(pan, out_dt)
         bands_t = [_device.to_device(b, out_dt) for b in resampled]

@@ -474,3 +474,23 @@ def test_exact_default_switch(golden_fusion):
     for b, o in enumerate(got):
         assert np.array_equal(o, g[f"{name}/daub4/out{b}"])
     assert np.array_equal(one, g[f"{name}/daub4/out0"])
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_exact_host_pipeline_strips(kname, dt):
+    """numpy inputs with exact=True go through the host strip pipeline
+    (wf_ctx_set_exact): strips of the default 512 rows with their
+    neighbours' halo rows (the wrap only at the plane's top and bottom),
+    bit-identical to the device-resident exact path and to the oracle."""
+    rng = np.random.default_rng(29)
+    pan = rng.uniform(0, 255, (1100, 264)).astype(dt)
+    bands = [rng.uniform(0, 255, (550, 132)).astype(dt) for _ in range(3)]
+    host = wf.fuse(pan, bands, wf.DwtReplace(KINDS[kname]), exact=True)
+    dev = wf.fuse(torch.from_numpy(pan).cuda(), [torch.from_numpy(b).cuda() for b in bands],
+                  wf.DwtReplace(KINDS[kname]), exact=True)
+    ref = O.fuse(pan, bands, kname)
+    for hst, d, r in zip(host, dev, ref):
+        assert isinstance(hst, np.ndarray) and hst.dtype == r.dtype
+        assert np.array_equal(hst, d.cpu().numpy())
+        assert np.array_equal(hst, r)
