@@ -697,6 +697,9 @@ constexpr int kQ2Prod = 1;               // producer warps
 constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
 constexpr int kQ2TrRows = 16;            // transpose chunk (rows of 32 lanes)
 
+#ifndef WF_QNR_F64CELL  // ERGAS 2x2 sums in float64 (1) or FP32 TwoSums (0)
+#define WF_QNR_F64CELL 1
+#endif
 #ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound)
 #define WF_Q2_STAGES 3
 #endif
@@ -1268,6 +1271,37 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const float dpd = 0.25f * ((S_ - kph) + (plo - kpl));
         lwp += dpd;
         lwpp = fmaf(dpd, dpd, lwpp);
+#if WF_QNR_F64CELL
+        // The own bands' exact 2x2 sums in float64, off the FP32 pipe (this
+        // kernel's bottleneck) onto the otherwise idle FP64 and conversion
+        // pipes: a column's two rows add exactly in float64, the partner
+        // lane's column arrives by shuffle, and e = S/4 - m is one rounding,
+        // like the reference's float64 degrade minus the band
+        // (metrics.py:31-42,117).
+        float ef[2 * HP];
+#pragma unroll
+        for (int m = 0; m < 2 * HP; ++m) {
+          if (m < H) {
+            const double own = (double)fv[0][m] + (double)fv[1][m];
+            const double oth = (double)fv[0][H + m] + (double)fv[1][H + m];
+            const double S = own + __shfl_xor_sync(0xffffffffu, oth, 1);
+            const float mv = (m & 1) ? raw[m >> 1].y : raw[m >> 1].x;
+            ef[m] = (float)fma(S, 0.25, -(double)mv);
+          } else {
+            ef[m] = 0.f;
+          }
+        }
+        const float2 dpd2 = make_float2(dpd, dpd);
+#pragma unroll
+        for (int j = 0; j < HP; ++j) {
+          const float2 e = make_float2(ef[2 * j], ef[2 * j + 1]);
+          sse[j] = __ffma2_rn(e, e, sse[j]);
+          summ[j] = __fadd2_rn(summ[j], raw[j]);
+          const float2 dm = __fadd2_rn(raw[j], neg2(kml[j]));
+          lw1[j] = __fadd2_rn(lw1[j], dm);
+          lw2[j] = __ffma2_rn(dm, dm, lw2[j]);
+          lw3[j] = __ffma2_rn(dm, dpd2, lw3[j]);
+#else
         // per-column vertical TwoSums of every band (band pairs), then the
         // partner's columns for this lane's own bands (local m < H)
         float2 sv[NBE / 2], tv[NBE / 2];
@@ -1299,6 +1333,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
           lw1[j] = __fadd2_rn(lw1[j], dm);
           lw2[j] = __ffma2_rn(dm, dm, lw2[j]);
           lw3[j] = __ffma2_rn(dm, dpd2, lw3[j]);
+#endif
         }
         }
       }
