@@ -291,23 +291,28 @@ def _u8_device(x) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(np.asarray(x), dtype=np.uint8)).to(dev)
 
 
-def fuse_tile_quantized(pan_u8, ms_u8, method: FusionMethod):
+def fuse_tile_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = None):
     """tiling.py:163-172: fuse one self-contained 8 bpp tile in float32 (the
-    worker's computation, cluster.py:297-299); returns float32 planes."""
+    worker's computation, cluster.py:297-299); returns float32 planes.
+    exact=True: the reference's float64 sequence, so the planes (and their
+    quantisation) are the reference worker's bits."""
     pan_f = _u8_to_f32_dev(_u8_device(pan_u8))
     ms_f = [_u8_to_f32_dev(_u8_device(b)) for b in ms_u8]
-    out = fuse(pan_f, ms_f, method)
+    out = fuse(pan_f, ms_f, method, exact=exact)
     return out if _is_tensor(pan_u8) else [o.cpu().numpy() for o in out]
 
 
-def fuse_quantized(pan_u8, ms_u8, method: FusionMethod):
+def fuse_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = None):
     """[quantize(p) for p in fuse_tile_quantized(pan_u8, ms_u8, method)]
     (tiling.py:268-269) in ONE pass: uint8 PAN/MS in, uint8 out, float32
     arithmetic with the quantize fused into the store (2.25 + 1.25 B per PAN
     px per band instead of 9). Haar is bit-identical to the reference; D4 can
     differ by one LSB where a value lies within ~1e-4 of a .5 boundary.
     Shapes the 8 bpp kernels do not cover (MS not half size, W % 16 / 32)
-    take the float32 kernels plus the GPU quantize."""
+    take the float32 kernels plus the GPU quantize. exact=True (D4): the
+    reference-exact float64 sequence, then the quantize -- the reference
+    worker's bytes exactly (Haar's one-pass kernel already is)."""
+    exact = _exact(exact)
     if not isinstance(method, DwtReplace):
         raise TypeError(f"unknown fusion method {method!r}")
     is_t = _is_tensor(pan_u8)
@@ -320,7 +325,8 @@ def fuse_quantized(pan_u8, ms_u8, method: FusionMethod):
         raise OddDimension(f"panchromatic plane {w}x{h} has an odd dimension")
     half = (h // 2, w // 2)
     fast = all(_shape(b) == half for b in bands) and (
-        w % 16 == 0 if method.kind is WaveletKind.HAAR else w % 32 == 0)
+        w % 16 == 0 if method.kind is WaveletKind.HAAR else w % 32 == 0) and not (
+        exact and method.kind is WaveletKind.DAUB4)
     if fast:
         _check_min(h, w, method.kind)
         lib = _native.load()
@@ -342,7 +348,8 @@ def fuse_quantized(pan_u8, ms_u8, method: FusionMethod):
                 ctx, code, pan_c.ctypes.data, _native.ptr_array([b.ctypes.data for b in band_c]),
                 _native.ptr_array([o.ctypes.data for o in outs]), len(bands), h, w))
         return outs
-    fused = fuse_tile_quantized(_u8_device(pan_u8), [_u8_device(b) for b in bands], method)
+    fused = fuse_tile_quantized(_u8_device(pan_u8), [_u8_device(b) for b in bands], method,
+                                exact=exact)
     outs = [_quantize_dev(f) for f in fused]
     return outs if is_t else [o.cpu().numpy() for o in outs]
 

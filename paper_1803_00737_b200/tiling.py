@@ -203,14 +203,14 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
 
         pan_u8 = to_u8(pan)
         ms_u8 = [to_u8(b) for b in low]
-        if _u8_windows_ok(grid, kind):
+        if _u8_windows_ok(grid, kind) and not (exact and kind is WaveletKind.DAUB4):
             outs = [torch.empty_like(pan_u8) for _ in ms_u8]
             _window_fuse(kind, pan_u8, ms_u8, outs, grid)
-        else:  # same arithmetic through the float32 kernels + quantize
+        else:  # the float32 (or, exact, the reference's float64) kernels + quantize
             pan_f = _u8_to_f32_dev(pan_u8)
             ms_f = [_u8_to_f32_dev(b) for b in ms_u8]
             fo = [torch.empty_like(pan_f) for _ in ms_f]
-            _window_fuse(kind, pan_f, ms_f, fo, grid)
+            _window_fuse(kind, pan_f, ms_f, fo, grid, exact=exact)
             outs = [_quantize_dev(f) for f in fo]
         return outs if is_t else [o.cpu().numpy() for o in outs]
 

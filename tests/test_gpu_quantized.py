@@ -181,3 +181,20 @@ def test_u8_d4_equals_quantized_f32_kernel(shape, nb, variant, monkeypatch):
                   [torch.from_numpy(x.astype(np.float32)).cuda() for x in ms], m)
     for g, f in zip(got, f32):
         assert np.array_equal(g.cpu().numpy(), wf.quantize(f.cpu().numpy()))
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+def test_golden_tiles_exact_mode_bit_exact(kname):
+    """exact=True: the 8 bpp path runs the reference's float64 sequence, then
+    the quantize -- every golden tile's bytes equal the reference worker's
+    (tiling.py:163-172 + imageio.py:115-123), D4 included."""
+    for k in range(4):
+        nb = sum(1 for key in G.files if key.startswith(f"t{k}/ms"))
+        pan = G[f"t{k}/pan"]
+        ms = [G[f"t{k}/ms{b}"] for b in range(nb)]
+        got = wf.fuse_quantized(pan, ms, wf.DwtReplace(KINDS[kname]), exact=True)
+        for b, o in enumerate(got):
+            assert np.array_equal(o, G[f"t{k}/{kname}/out{b}"]), (k, b)
+        f32 = wf.fuse_tile_quantized(pan, ms, wf.DwtReplace(KINDS[kname]), exact=True)
+        for b, o in enumerate(f32):
+            assert np.array_equal(wf.quantize(o), G[f"t{k}/{kname}/out{b}"]), (k, b)
