@@ -134,6 +134,16 @@ def _fuse_device(pan_t: torch.Tensor, bands_t: list[torch.Tensor], kind: Wavelet
     return outs
 
 
+def _host_out(shape, dt) -> np.ndarray:
+    """A fresh numpy output. WF_PINNED_OUT=1: backed by page-locked memory from
+    torch's caching host allocator (the D2H lands in it directly, no staging
+    copy; the block returns to the cache when the array is freed)."""
+    if os.environ.get("WF_PINNED_OUT") == "1":
+        tdt = torch.float32 if np.dtype(dt) == np.float32 else torch.float64
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    return np.empty(shape, dtype=dt)
+
+
 def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
                out_dt, exact: bool = False) -> list[np.ndarray]:
     """All bands through the library's host-buffer pipeline (H2D / fuse / D2H
@@ -142,7 +152,7 @@ def _fuse_host(pan: np.ndarray, bands: list[np.ndarray], kind: WaveletKind,
     h, w = pan.shape
     pan_c = np.ascontiguousarray(pan, dtype=out_dt)
     band_c = [np.ascontiguousarray(b, dtype=out_dt) for b in bands]
-    outs = [np.empty((h, w), dtype=out_dt) for _ in bands]
+    outs = [_host_out((h, w), out_dt) for _ in bands]
     lib = _native.load()
     fn = lib.wf_fuse_host_f32 if out_dt == np.float32 else lib.wf_fuse_host_f64
     ms_ptrs = _native.ptr_array([b.ctypes.data for b in band_c])

@@ -17,7 +17,7 @@ ms = [synth.hash_plane(42, 1 + b, np.arange(H // 2), np.arange(W // 2)) for b in
 for kind in (wf.WaveletKind.HAAR, wf.WaveletKind.DAUB4):
     m = wf.DwtReplace(kind)
     wf.fuse(pan[:512], [b[:256] for b in ms], m)
-    for rep in range(3):
+    for rep in range(4):
         t0 = time.perf_counter()
         wf.fuse(pan, ms, m)
         dt = time.perf_counter() - t0
