@@ -109,6 +109,19 @@ int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const doub
                       const double* pan_bot, int64_t halo_pitch, const double* const* ms,
                       const double* const* ms_top, int64_t ms_pitch, double* const* out,
                       int64_t out_pitch, int nbands, int rows, int w, void* stream);
+/* The same strip in the reference-exact sequence (the one-pass float64
+ * kernels reading the halo rows, which may live in a neighbour GPU's HBM):
+ * the strips of a scene are bit-identical to the reference's whole-scene
+ * fuse_dwt. */
+int wf_fuse_strip_exact_f32(int kind, const float* pan, int64_t pan_pitch, const float* pan_top,
+                            const float* pan_bot, int64_t halo_pitch, const float* const* ms,
+                            const float* const* ms_top, int64_t ms_pitch, float* const* out,
+                            int64_t out_pitch, int nbands, int rows, int w, void* stream);
+int wf_fuse_strip_exact_f64(int kind, const double* pan, int64_t pan_pitch,
+                            const double* pan_top, const double* pan_bot, int64_t halo_pitch,
+                            const double* const* ms, const double* const* ms_top,
+                            int64_t ms_pitch, double* const* out, int64_t out_pitch, int nbands,
+                            int rows, int w, void* stream);
 
 /* Reference-exact fuse_dwt (fusion.py:148-150 step by step): float64
  * forward transform in the reference's operation order, LL <- band * gain,

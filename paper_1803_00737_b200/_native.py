@@ -57,6 +57,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         sig[f"wf_fuse_strip_{t}"] = [c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vpp, c_vpp, c_i64,
                                      c_vpp, c_i64, c_int, c_int, c_int, c_vp]
         sig[f"wf_fuse_host_{t}"] = [c_vp, c_int, c_vp, c_vpp, c_vpp, c_int, c_int, c_int]
+        sig[f"wf_fuse_strip_exact_{t}"] = sig[f"wf_fuse_strip_{t}"]
         for d in ("forward", "inverse"):
             sig[f"wf_dwt2d_{d}_{t}"] = [c_int, c_vp, c_i64, c_vp, c_i64, c_int, c_int, c_vp]
             sig[f"wf_dwt_rows_{d}_{t}"] = [c_int, c_vp, c_i64, c_vp, c_i64, c_int, c_int, c_vp]

@@ -529,6 +529,23 @@ int wf_fuse_strip_f64(int kind, const double* pan, int64_t pan_pitch, const doub
                              ms_pitch, out, out_pitch, nbands, rows, w, true,
                              (cudaStream_t)stream);
 }
+int wf_fuse_strip_exact_f32(int kind, const float* pan, int64_t pan_pitch, const float* pan_top,
+                            const float* pan_bot, int64_t halo_pitch, const float* const* ms,
+                            const float* const* ms_top, int64_t ms_pitch, float* const* out,
+                            int64_t out_pitch, int nbands, int rows, int w, void* stream) {
+  return fuse_common<float>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
+                            ms_pitch, out, out_pitch, nbands, rows, w, true,
+                            (cudaStream_t)stream, true);
+}
+int wf_fuse_strip_exact_f64(int kind, const double* pan, int64_t pan_pitch,
+                            const double* pan_top, const double* pan_bot, int64_t halo_pitch,
+                            const double* const* ms, const double* const* ms_top,
+                            int64_t ms_pitch, double* const* out, int64_t out_pitch, int nbands,
+                            int rows, int w, void* stream) {
+  return fuse_common<double>(kind, pan, pan_pitch, pan_top, pan_bot, halo_pitch, ms, ms_top,
+                             ms_pitch, out, out_pitch, nbands, rows, w, true,
+                             (cudaStream_t)stream, true);
+}
 
 int wf_ctx_set_exact(wf_ctx* ctx, int exact) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");

@@ -155,14 +155,20 @@ def _halo_pointers(halos):
 
 
 def fuse_strip(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
-               halos=None, out: list[torch.Tensor] | None = None) -> list[torch.Tensor]:
+               halos=None, out: list[torch.Tensor] | None = None, *,
+               exact: bool = False) -> list[torch.Tensor]:
     """Fuse one row strip on this rank's GPU through wf_fuse_strip_*.
-    `halos` = exchange_halos(...) tensors or a PeerHalos mapping (D4)."""
+    `halos` = exchange_halos(...) tensors or a PeerHalos mapping (D4).
+    exact=True: wf_fuse_strip_exact_* (the reference's float64 sequence; the
+    strips of a scene are bit-identical to the reference's whole scene)."""
     rows, w = pan.shape
     if out is None:
         out = [torch.empty_like(pan) for _ in ms]
     lib = _native.load()
-    fn = lib.wf_fuse_strip_f32 if pan.dtype == torch.float32 else lib.wf_fuse_strip_f64
+    if exact:
+        fn = lib.wf_fuse_strip_exact_f32 if pan.dtype == torch.float32 else lib.wf_fuse_strip_exact_f64
+    else:
+        fn = lib.wf_fuse_strip_f32 if pan.dtype == torch.float32 else lib.wf_fuse_strip_f64
     if kind is WaveletKind.DAUB4:
         top_p, bot_p, hp, mtops = _halo_pointers(halos)
         mtop_p = _native.ptr_array(mtops)
@@ -178,7 +184,7 @@ def fuse_strip(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor],
 
 
 def fuse_scene_strips(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tensor], group=None,
-                      compute: Callable | None = None):
+                      compute: Callable | None = None, *, exact: bool = False):
     """This rank's share of a strip-sharded scene: halo exchange (D4 only),
     then the strip kernel. `compute(kind, pan, ms, halos)` replaces the GPU
     kernel in CPU-only tests of the exchange logic (tests inject the oracle);
@@ -186,4 +192,4 @@ def fuse_scene_strips(kind: WaveletKind, pan: torch.Tensor, ms: list[torch.Tenso
     halos = exchange_halos(pan, ms, group) if kind is WaveletKind.DAUB4 else None
     if compute is not None:
         return compute(kind, pan, ms, halos)
-    return fuse_strip(kind, pan, ms, halos)
+    return fuse_strip(kind, pan, ms, halos, exact=exact)

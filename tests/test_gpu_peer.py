@@ -40,10 +40,13 @@ def _worker(rank, world, port, outdir):
         dist.barrier()  # every strip's inputs exist before anyone maps them
         halos = strips.PeerHalos(pan, ms)
         out = strips.fuse_strip(wf.WaveletKind.DAUB4, pan, ms, halos)
+        # the reference-exact strip kernel reads the same peer halo rows
+        ex = strips.fuse_strip(wf.WaveletKind.DAUB4, pan, ms, halos, exact=True)
         torch.cuda.synchronize()
         dist.barrier()  # neighbours are done reading before mappings go away
         halos.close()
         np.save(os.path.join(outdir, f"r{rank}.npy"), np.stack([o.cpu().numpy() for o in out]))
+        np.save(os.path.join(outdir, f"x{rank}.npy"), np.stack([o.cpu().numpy() for o in ex]))
     finally:
         dist.destroy_process_group()
 
@@ -67,6 +70,12 @@ def test_peer_halos_two_processes(tmp_path):
     got = np.concatenate([np.load(tmp_path / f"r{r}.npy") for r in range(2)], axis=1)
     for b in range(B):
         assert np.array_equal(got[b], want[b])
+    # exact strips across ranks == the exact whole scene (the reference's bits)
+    want_x = [o.cpu().numpy() for o in wf.fuse(pan, ms, wf.DwtReplace(wf.WaveletKind.DAUB4),
+                                               exact=True)]
+    got_x = np.concatenate([np.load(tmp_path / f"x{r}.npy") for r in range(2)], axis=1)
+    for b in range(B):
+        assert np.array_equal(got_x[b], want_x[b])
 
 
 def test_peer_halos_single_rank_wraps_locally():
