@@ -174,6 +174,31 @@ def cpu_sample(kind_name: str, rows: int, threads: int, reps: int = 1):
     return rows * W / 1e6 / t, t
 
 
+def cpu_sample_shape(kind_name: str, rows: int, width: int, bands: int, threads: int,
+                     with_qnr: bool = False):
+    """The oracle port on `rows` x `width` PAN rows (+ `bands` MS bands) of the
+    synthetic scene, fused with exact strip parallelism over `threads`, and
+    optionally scored by the oracle's qnr (metrics.py:178-199, single
+    thread). Returns (PAN MPix/s, seconds)."""
+    import numpy as np
+
+    from oracle import cpu_dwt as O
+    from oracle import cpu_quality as Q
+    from paper_1803_00737_b200 import synth
+
+    r = np.arange(rows)
+    pan = synth.hash_plane(synth.DEFAULT_SEED, synth.plane_id(0, -1), r, np.arange(width))
+    ms = [synth.hash_plane(synth.DEFAULT_SEED, synth.plane_id(0, b), r[: rows // 2],
+                           np.arange(width // 2)) for b in range(bands)]
+    t0 = time.perf_counter()
+    fused = O.fuse_parallel(pan, ms, kind_name, threads=threads,
+                            strip_rows=max(64, rows // threads))
+    if with_qnr:
+        Q.qnr(fused, ms, pan)
+    t = time.perf_counter() - t0
+    return rows * width / 1e6 / t, t
+
+
 def run_reference(args, rank: int):
     if rank != 0:
         return
@@ -871,6 +896,16 @@ def run_strips(args, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": strip_bytes,
                          "note": "per-rank strip bytes / per-step time (halo exchange included)"},
         }
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rows = 512
+            rate, t = cpu_sample_shape("daub4", rows, n, 1, threads)
+            line["cpu_baseline"] = {
+                "value": round(rate, 3), "unit": "scene-MPix/s", "cores": threads, "kind": "port",
+                "sample": (f"first {rows} PAN rows x {n} cols + 1 band of the C4 scene, D4, oracle "
+                           f"port of the reference (numpy f64, exact row strips), {t:.2f} s; a "
+                           "per-pixel rate, so no extrapolation to the full scene"),
+            }
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -961,6 +996,16 @@ def run_batch(args, rank, world, local_rank):
             "clocks": clk.summary(),
             "qnr_sample": round(float(sum(reports) / max(1, len(reports))), 6),
         }
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rows = 512
+            rate, t = cpu_sample_shape("haar", rows, W, B, threads, with_qnr=True)
+            line["cpu_baseline"] = {
+                "value": round(rate, 4), "unit": line["unit"], "cores": threads, "kind": "port",
+                "sample": (f"first {rows} PAN rows x {W} cols + {B} bands of one scene, Haar "
+                           f"fused (oracle port, {threads} threads) and scored (oracle qnr, one "
+                           f"thread), {t:.1f} s; per-pixel rate of one scene-wavelet pass"),
+            }
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
