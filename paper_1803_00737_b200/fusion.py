@@ -171,7 +171,9 @@ def _fuse_exact_device(pan_t: torch.Tensor, bands_t: list[torch.Tensor], kind: W
     cast -- bit-identical to fusion.py:148-150."""
     h, w = pan_t.shape
     lib = _native.load()
-    ws = torch.empty((h, w), dtype=torch.float64, device=pan_t.device)
+    # the workspace is only used by the WF_EXACT_TRANSFORMS=1 kernel sequence
+    ws = torch.empty((h, w) if os.environ.get("WF_EXACT_TRANSFORMS") else (1,),
+                     dtype=torch.float64, device=pan_t.device)
     outs = [torch.empty((h, w), dtype=pan_t.dtype, device=pan_t.device) for _ in bands_t]
     if len(bands_t) == 1:  # fuse_dwt: the per-band entry point
         fn = lib.wf_fuse_dwt_exact_f32 if out_dt == np.float32 else lib.wf_fuse_dwt_exact_f64
