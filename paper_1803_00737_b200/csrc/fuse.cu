@@ -27,6 +27,10 @@
 // a halo-aware row source, so the same kernel serves whole images (halos alias
 // the wrapped rows of the image itself) and row strips whose halo rows arrived
 // from neighbouring GPUs (strips.py).
+#include <stdlib.h>
+
+#include <type_traits>
+
 #include "wf_common.cuh"
 #include "wf_kernels.h"
 
@@ -257,7 +261,7 @@ constexpr int kHaarThreads = 128;
 // one row pair per thread measured best (tools/sweep_haar.py: 6.56 TB/s at
 // B = 6 vs 6.28 at 4 pairs) -- more, shorter-lived warps keep more loads in flight
 constexpr int kHaarPairsPerThread = 1;
-constexpr int kHaarU8PairsPerThread = 4;
+constexpr int kHaarU8PairsPerThread = 1;  // WF_HAAR_U8_PPT sweep: 1 -> 0.296 ms, 4 -> 0.317, 8 -> 0.330
 
 template <typename T, typename Acc, int NB, bool kVec, int PPT>
 __global__ void __launch_bounds__(kHaarThreads)
@@ -433,16 +437,16 @@ __device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t ma
   return r;
 }
 
-template <int NB>
+template <int NB, int PPT = kHaarU8PairsPerThread>
 __global__ void __launch_bounds__(kHaarThreads)
     fuse_haar_u8_kernel(const FuseArgs<uint8_t> a) {
   const int g = blockIdx.x * kHaarThreads + threadIdx.x;  // 16-column group
   const int c = 16 * g;
   if (c >= a.W) return;
   const int npairs = a.rows >> 1;
-  const int i_begin = blockIdx.y * kHaarU8PairsPerThread;
+  const int i_begin = blockIdx.y * PPT;
 #pragma unroll
-  for (int s = 0; s < kHaarU8PairsPerThread; ++s) {
+  for (int s = 0; s < PPT; ++s) {
     const int i = i_begin + s;
     if (i >= npairs) break;
     const uint8_t* r0 = a.pan + (long long)(2 * i) * a.pan_pitch + c;
@@ -502,9 +506,19 @@ __global__ void __launch_bounds__(kHaarThreads)
 template <int NB>
 static cudaError_t launch_haar_u8(const FuseArgs<uint8_t>& a, cudaStream_t s) {
   const int ng = (a.W + 15) / 16;
-  dim3 grid((ng + kHaarThreads - 1) / kHaarThreads,
-            ((a.rows >> 1) + kHaarU8PairsPerThread - 1) / kHaarU8PairsPerThread);
-  fuse_haar_u8_kernel<NB><<<grid, kHaarThreads, 0, s>>>(a);
+  int ppt = kHaarU8PairsPerThread;
+  if (const char* e = getenv("WF_HAAR_U8_PPT")) ppt = atoi(e) > 0 ? atoi(e) : ppt;
+  auto go = [&](auto P) {
+    constexpr int kP = decltype(P)::value;
+    dim3 grid((ng + kHaarThreads - 1) / kHaarThreads, ((a.rows >> 1) + kP - 1) / kP);
+    fuse_haar_u8_kernel<NB, kP><<<grid, kHaarThreads, 0, s>>>(a);
+  };
+  switch (ppt) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 8: go(std::integral_constant<int, 8>{}); break;
+    default: go(std::integral_constant<int, 4>{}); break;
+  }
   return cudaGetLastError();
 }
 
