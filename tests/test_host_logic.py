@@ -136,3 +136,29 @@ def test_plan_grid_contract():
         wf.fuse_tiled(np.ones((8, 8)), [np.ones((4, 4))], wf.DwtReplace(H), g)
     with pytest.raises(ValueError):
         wf.fuse_tiled(np.ones((32, 64)), [np.ones((16, 32))], wf.DwtReplace(H), g, workers=0)
+
+
+def test_exact_default_switch_logic(monkeypatch):
+    """The `exact` keyword defaults to the module switch (WF_EXACT /
+    set_exact_default); an explicit True/False always wins."""
+    from paper_1803_00737_b200 import fusion
+
+    monkeypatch.setattr(fusion, "_EXACT_DEFAULT", False)
+    assert fusion._exact(None) is False and fusion._exact(True) is True
+    wf.set_exact_default(True)
+    try:
+        assert fusion._exact(None) is True and fusion._exact(False) is False
+    finally:
+        wf.set_exact_default(False)
+    assert fusion._exact(None) is False
+
+
+def test_exact_keyword_validates_before_compute():
+    """exact=True keeps the reference's precondition order and exceptions
+    (fusion.py:137-147): no GPU is touched before they are raised."""
+    with pytest.raises(wf.errors.OddDimension):
+        wf.fuse(np.ones((5, 8)), [np.ones((2, 4))], wf.DwtReplace(wf.WaveletKind.HAAR), exact=True)
+    with pytest.raises(wf.errors.DimensionMismatch):
+        wf.fuse_dwt(np.ones((8, 8)), np.ones((3, 4)), wf.WaveletKind.DAUB4, exact=True)
+    with pytest.raises(wf.errors.TooSmall):
+        wf.fuse_dwt(np.ones((2, 8)), np.ones((1, 4)), wf.WaveletKind.DAUB4, exact=True)
