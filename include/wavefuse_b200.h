@@ -161,6 +161,12 @@ wf_ctx* wf_ctx_create(int device, int strip_rows);
  * halo rows) -- bit-identical host-buffer fusion at PCIe speed. u8 calls are
  * unaffected. */
 int wf_ctx_set_exact(wf_ctx* ctx, int exact);
+/* Host -> device copy of `bytes` from a (pageable or pinned) host buffer
+ * through the context's pinned staging and copy workers; `after` is the
+ * stream whose earlier work must finish before dst is written. Synchronous.
+ * What the Python layer uses to bring numpy planes to the device for the
+ * metrics (metrics.py's inputs) at the host-memcpy / PCIe rate. */
+int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after);
 void wf_ctx_destroy(wf_ctx* ctx);
 int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const* ms,
                      float* const* out, int nbands, int h, int w);

@@ -17,6 +17,7 @@ import torch
 
 from . import _native
 
+_UPLOAD_MIN = 8 << 20  # bytes; smaller planes go through torch's copy
 _ctxs: list[int] = []
 _free: list[int] = []
 _ctx_lock = threading.Lock()
@@ -58,7 +59,14 @@ def to_device(x, np_dtype) -> torch.Tensor:
         t = x if x.is_cuda else x.to(dev)
         return t.to(tdt).contiguous()
     arr = np.ascontiguousarray(np.asarray(x), dtype=np_dtype)
-    return torch.from_numpy(arr).to(dev)
+    if arr.nbytes < _UPLOAD_MIN:
+        return torch.from_numpy(arr).to(dev)
+    # large planes: the library's staged, multi-threaded upload (wf_ctx_upload)
+    t = torch.empty(arr.shape, dtype=tdt, device=dev)
+    with host_ctx() as ctx:
+        _native.check(_native.load().wf_ctx_upload(ctx, t.data_ptr(), arr.ctypes.data, arr.nbytes,
+                                                   stream_ptr()))
+    return t
 
 
 def stream_ptr() -> int:

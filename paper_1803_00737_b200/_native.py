@@ -93,6 +93,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.wf_launch_count.restype = c_i64
     lib.wf_ctx_create.argtypes = [c_int, c_int]
     lib.wf_ctx_create.restype = c_vp
+    lib.wf_ctx_upload.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp]
+    lib.wf_ctx_upload.restype = c_int
     lib.wf_ctx_set_exact.argtypes = [c_vp, c_int]
     lib.wf_ctx_set_exact.restype = c_int
     lib.wf_ctx_destroy.argtypes = [c_vp]

@@ -547,6 +547,54 @@ int wf_fuse_strip_exact_f64(int kind, const double* pan, int64_t pan_pitch,
                              (cudaStream_t)stream, true);
 }
 
+// Host -> device copy of a (pageable) host buffer through the context's
+// pinned staging slots: 32 MiB chunks, the copy workers filling one slot while
+// the DMA of the previous ones runs (torch's pageable .to(device) moves ~11
+// GB/s; this path runs at the host-memcpy / PCIe rate). `after` = the stream
+// whose earlier work must complete before `dst` is written (the allocating
+// stream). Returns when the data is on the device.
+int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
+  if (!ctx) return fail(WF_ERR_VALUE, "null context");
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(WF_ERR_VALUE, "bad upload arguments");
+  if (bytes == 0) return WF_OK;
+  if (cudaError_t e = cudaSetDevice(ctx->device)) return cuda_status(e, "cudaSetDevice");
+  if (cudaError_t e = cudaStreamSynchronize((cudaStream_t)after)) return cuda_status(e, "sync");
+  if (is_pinned(src)) {
+    cudaStream_t st = ctx->slot[0].stream;
+    cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return cuda_status(e, "upload");
+  }
+  if (!ctx->pool) ctx->pool.reset(new CopyPool(copy_threads()));
+  constexpr size_t kChunk = 32u << 20;
+  for (int k = 0; k < kSlots; ++k) {
+    Slot& sl = ctx->slot[k];
+    if (sl.hbytes < kChunk) {
+      if (sl.hbuf) cudaFreeHost(sl.hbuf);
+      sl.hbuf = nullptr;
+      sl.hbytes = 0;
+      if (cudaError_t e = cudaHostAlloc(&sl.hbuf, kChunk, cudaHostAllocPortable))
+        return cuda_status(e, "cudaHostAlloc staging");
+      sl.hbytes = kChunk;
+    }
+    sl.pend_r0 = -1;
+  }
+  cudaError_t e = cudaSuccess;
+  int k = 0;
+  for (size_t off = 0; off < (size_t)bytes && e == cudaSuccess; off += kChunk, k = (k + 1) % kSlots) {
+    Slot& sl = ctx->slot[k];
+    const size_t n = (size_t)bytes - off < kChunk ? (size_t)bytes - off : kChunk;
+    e = cudaEventSynchronize(sl.done);  // the slot's previous DMA has read its staging
+    if (e != cudaSuccess) break;
+    ctx->pool->copy({{sl.hbuf, static_cast<const char*>(src) + off, n}});
+    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, sl.hbuf, n, cudaMemcpyHostToDevice,
+                        sl.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(sl.done, sl.stream);
+  }
+  for (int j = 0; j < kSlots && e == cudaSuccess; ++j) e = cudaStreamSynchronize(ctx->slot[j].stream);
+  return cuda_status(e, "upload");
+}
+
 int wf_ctx_set_exact(wf_ctx* ctx, int exact) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   ctx->exact = exact ? 1 : 0;
