@@ -167,6 +167,9 @@ int wf_ctx_set_exact(wf_ctx* ctx, int exact);
  * What the Python layer uses to bring numpy planes to the device for the
  * metrics (metrics.py's inputs) at the host-memcpy / PCIe rate. */
 int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after);
+/* Device -> host counterpart of wf_ctx_upload (`after` = the stream that
+ * produced src). Synchronous. */
+int wf_ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after);
 void wf_ctx_destroy(wf_ctx* ctx);
 int wf_fuse_host_f32(wf_ctx* ctx, int kind, const float* pan, const float* const* ms,
                      float* const* out, int nbands, int h, int w);

@@ -69,6 +69,20 @@ def to_device(x, np_dtype) -> torch.Tensor:
     return t
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """A CUDA tensor as a fresh numpy array (`.cpu().numpy()`); planes of 8 MB
+    and more come down through the library's staged, multi-threaded
+    download (wf_ctx_download)."""
+    if not t.is_cuda or t.numel() * t.element_size() < _UPLOAD_MIN:
+        return t.cpu().numpy()
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=np.dtype(str(t.dtype).replace("torch.", "")))
+    with host_ctx() as ctx:
+        _native.check(_native.load().wf_ctx_download(ctx, out.ctypes.data, t.data_ptr(),
+                                                     out.nbytes, stream_ptr()))
+    return out
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 

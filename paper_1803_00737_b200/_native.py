@@ -95,6 +95,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.wf_ctx_create.restype = c_vp
     lib.wf_ctx_upload.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp]
     lib.wf_ctx_upload.restype = c_int
+    lib.wf_ctx_download.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp]
+    lib.wf_ctx_download.restype = c_int
     lib.wf_ctx_set_exact.argtypes = [c_vp, c_int]
     lib.wf_ctx_set_exact.restype = c_int
     lib.wf_ctx_destroy.argtypes = [c_vp]

@@ -595,6 +595,55 @@ int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* 
   return cuda_status(e, "upload");
 }
 
+// Device -> host counterpart: up to kSlots 32 MiB DMAs in flight into the
+// pinned staging while the copy workers move finished chunks to `dst`.
+// `after` = the stream that produced src. Synchronous.
+int wf_ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
+  if (!ctx) return fail(WF_ERR_VALUE, "null context");
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(WF_ERR_VALUE, "bad download arguments");
+  if (bytes == 0) return WF_OK;
+  if (cudaError_t e = cudaSetDevice(ctx->device)) return cuda_status(e, "cudaSetDevice");
+  if (cudaError_t e = cudaStreamSynchronize((cudaStream_t)after)) return cuda_status(e, "sync");
+  if (is_pinned(dst)) {
+    cudaStream_t st = ctx->slot[0].stream;
+    cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return cuda_status(e, "download");
+  }
+  if (!ctx->pool) ctx->pool.reset(new CopyPool(copy_threads()));
+  constexpr size_t kChunk = 32u << 20;
+  for (int k = 0; k < kSlots; ++k) {
+    Slot& sl = ctx->slot[k];
+    if (sl.hbytes < kChunk) {
+      if (sl.hbuf) cudaFreeHost(sl.hbuf);
+      sl.hbuf = nullptr;
+      sl.hbytes = 0;
+      if (cudaError_t e = cudaHostAlloc(&sl.hbuf, kChunk, cudaHostAllocPortable))
+        return cuda_status(e, "cudaHostAlloc staging");
+      sl.hbytes = kChunk;
+    }
+    sl.pend_r0 = -1;
+  }
+  const size_t total = (size_t)bytes, nchunks = (total + kChunk - 1) / kChunk;
+  auto len = [&](size_t c) { return total - c * kChunk < kChunk ? total - c * kChunk : kChunk; };
+  cudaError_t e = cudaSuccess;
+  auto issue = [&](size_t c) {
+    Slot& sl = ctx->slot[c % kSlots];
+    e = cudaMemcpyAsync(sl.hbuf, static_cast<const char*>(src) + c * kChunk, len(c),
+                        cudaMemcpyDeviceToHost, sl.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(sl.done, sl.stream);
+  };
+  for (size_t c = 0; c < nchunks && c < (size_t)kSlots && e == cudaSuccess; ++c) issue(c);
+  for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    Slot& sl = ctx->slot[c % kSlots];
+    e = cudaEventSynchronize(sl.done);
+    if (e != cudaSuccess) break;
+    ctx->pool->copy({{static_cast<char*>(dst) + c * kChunk, sl.hbuf, len(c)}});
+    if (c + kSlots < nchunks) issue(c + kSlots);
+  }
+  return cuda_status(e, "download");
+}
+
 int wf_ctx_set_exact(wf_ctx* ctx, int exact) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   ctx->exact = exact ? 1 : 0;

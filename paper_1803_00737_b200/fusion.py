@@ -95,7 +95,7 @@ def resample_bilinear(plane, out_w: int, out_h: int):
     fn = lib.wf_resample_bilinear_f32 if dt == np.float32 else lib.wf_resample_bilinear_f64
     _native.check(fn(d_in.data_ptr(), in_w, in_h, in_w, d_out.data_ptr(), out_w, out_h, out_w,
                      _device.stream_ptr()))
-    return d_out if _is_tensor(plane) else d_out.cpu().numpy()
+    return d_out if _is_tensor(plane) else _device.to_host(d_out)
 
 
 # ---------------------------------------------------------------------------
@@ -252,7 +252,7 @@ def fuse(pan, ms, method: FusionMethod, *, exact: bool | None = None):
         outs = _fuse_exact_device(_device.to_device(pan, out_dt),
                                   [_device.to_device(b, out_dt) for b in resampled],
                                   method.kind, out_dt)
-        return outs if _is_tensor(pan) else [o.cpu().numpy() for o in outs]
+        return outs if _is_tensor(pan) else [_device.to_host(o) for o in outs]
     if exact:  # host buffers: the strip pipeline with the exact kernels
         return _fuse_host(pan, [np.asarray(b) for b in resampled], method.kind, out_dt,
                           exact=True)
@@ -260,7 +260,7 @@ def fuse(pan, ms, method: FusionMethod, *, exact: bool | None = None):
         pan_t = _device.to_device(pan, out_dt)
         bands_t = [_device.to_device(b, out_dt) for b in resampled]
         outs = _fuse_device(pan_t, bands_t, method.kind, out_dt)
-        return outs if _is_tensor(pan) else [o.cpu().numpy() for o in outs]
+        return outs if _is_tensor(pan) else [_device.to_host(o) for o in outs]
     return _fuse_host(pan, resampled, method.kind, out_dt)
 
 
@@ -293,7 +293,7 @@ def quantize(plane):
     if t.dim() != 2:  # any shape: quantize is elementwise
         t = t.reshape(1, -1)
     out = _quantize_dev(t).reshape(shape)
-    return out if is_t else out.cpu().numpy()
+    return out if is_t else _device.to_host(out)
 
 
 def _u8_device(x) -> torch.Tensor:
@@ -311,7 +311,7 @@ def fuse_tile_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | No
     pan_f = _u8_to_f32_dev(_u8_device(pan_u8))
     ms_f = [_u8_to_f32_dev(_u8_device(b)) for b in ms_u8]
     out = fuse(pan_f, ms_f, method, exact=exact)
-    return out if _is_tensor(pan_u8) else [o.cpu().numpy() for o in out]
+    return out if _is_tensor(pan_u8) else [_device.to_host(o) for o in out]
 
 
 def fuse_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = None):
@@ -363,7 +363,7 @@ def fuse_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = 
     fused = fuse_tile_quantized(_u8_device(pan_u8), [_u8_device(b) for b in bands], method,
                                 exact=exact)
     outs = [_quantize_dev(f) for f in fused]
-    return outs if is_t else [o.cpu().numpy() for o in outs]
+    return outs if is_t else [_device.to_host(o) for o in outs]
 
 
 def method_from_name(name: str, weight: float = 0.5) -> FusionMethod:

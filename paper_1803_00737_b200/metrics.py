@@ -123,7 +123,7 @@ def degrade(plane, factor: int):
     if h % factor or w % factor:
         raise NotDivisible(f"{w}x{h} not divisible by {factor}")
     out = _degrade_dev(_plane(plane), factor)
-    return out if isinstance(plane, torch.Tensor) else out.cpu().numpy()
+    return out if isinstance(plane, torch.Tensor) else _device.to_host(out)
 
 
 def q_index(a, b) -> float:
@@ -462,6 +462,6 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
                 ws.data_ptr(), out.data_ptr(), flag.data_ptr(), _device.stream_ptr()))
             rep = (qnr(outs, m_t, p_t) if int(flag.item())
                    else _scene_report(out.cpu().numpy(), n, 2))
-            return (outs if is_t else [o.cpu().numpy() for o in outs]), rep
+            return (outs if is_t else [_device.to_host(o) for o in outs]), rep
     fused = _fusion.fuse(pan, ms, method)
     return fused, qnr(fused, ms, pan)

@@ -161,7 +161,7 @@ def to_plane(raster, channel: int = 0):
     if channel < 0 or channel >= channels:
         raise ChannelOutOfRange(f"channel {channel} of {channels}")
     out = _plane_dev(_raster_device(raster), channel)
-    return out if is_t else out.cpu().numpy()
+    return out if is_t else _device.to_host(out)
 
 
 def _raster_from_planes(planes: list[torch.Tensor], h: int, w: int) -> np.ndarray:
@@ -175,7 +175,7 @@ def _raster_from_planes(planes: list[torch.Tensor], h: int, w: int) -> np.ndarra
           else lib.wf_planes_to_raster_f64)
     _native.check(fn(_native.ptr_array([p.data_ptr() for p in planes]), np_, planes[0].stride(0),
                      h, w, raster.data_ptr(), _device.stream_ptr()))
-    return raster.cpu().numpy()
+    return _device.to_host(raster)
 
 
 def fuse_pnm(pan: bytes, ms: list[bytes], method: FusionMethod, grid: tuple[int, int] = (1, 1),

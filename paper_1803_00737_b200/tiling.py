@@ -101,7 +101,7 @@ def pad_edge(plane, out_w: int, out_h: int):
         fn = _native.load().wf_pad_edge_f32 if dt == np.float32 else _native.load().wf_pad_edge_f64
         _native.check(fn(src.data_ptr(), src.stride(0), h, w, out.data_ptr(), out_w, out_h, out_w,
                          _device.stream_ptr()))
-    return out if is_t else out.cpu().numpy()
+    return out if is_t else _device.to_host(out)
 
 
 def pad_inputs(pan, ms, grid_w: int, grid_h: int):
@@ -212,7 +212,7 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
             fo = [torch.empty_like(pan_f) for _ in ms_f]
             _window_fuse(kind, pan_f, ms_f, fo, grid, exact=exact)
             outs = [_quantize_dev(f) for f in fo]
-        return outs if is_t else [o.cpu().numpy() for o in outs]
+        return outs if is_t else [_device.to_host(o) for o in outs]
 
     dt = _device.np_out_dtype(pan)
     sized = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0]) for b in bands]
@@ -220,5 +220,5 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
     ms_t = [_device.to_device(b, dt) for b in sized]
     outs = [torch.empty_like(pan_t) for _ in ms_t]
     _window_fuse(kind, pan_t, ms_t, outs, grid, exact=exact)
-    return outs if is_t else [o.cpu().numpy() for o in outs]
+    return outs if is_t else [_device.to_host(o) for o in outs]
 

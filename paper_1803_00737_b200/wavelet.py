@@ -89,7 +89,7 @@ def check_2d(shape, kind: WaveletKind) -> None:
 
 
 def _finish(x, out: torch.Tensor):
-    return out if isinstance(x, torch.Tensor) else out.cpu().numpy()
+    return out if isinstance(x, torch.Tensor) else _device.to_host(out)
 
 
 def _rows_call(x, kind: WaveletKind, inverse: bool):
