@@ -45,3 +45,17 @@ t = lap("H2D of the scene (torch)", t)
 for rep in range(2):
     wf.qnr(fd, md, pd)
     t = lap(f"qnr device call {rep + 1}", t)
+# the rest of the numpy-facing API on the same scene
+grid = wf.plan_grid(W, H, 4, 2)
+for rep in range(2):
+    wf.fuse_tiled(pan, ms, wf.DwtReplace(wf.WaveletKind.DAUB4), grid)
+    t = lap(f"fuse_tiled numpy 4x2 D4 call {rep + 1}", t)
+for rep in range(2):
+    c = wf.dwt2d_forward(pan, wf.WaveletKind.DAUB4)
+    t = lap(f"dwt2d_forward numpy call {rep + 1}", t)
+for rep in range(2):
+    wf.dwt2d_inverse(c, wf.WaveletKind.DAUB4)
+    t = lap(f"dwt2d_inverse numpy call {rep + 1}", t)
+for rep in range(2):
+    wf.resample_bilinear(ms[0], W, H)
+    t = lap(f"resample_bilinear numpy 2x call {rep + 1}", t)
