@@ -463,5 +463,19 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
             rep = (qnr(outs, m_t, p_t) if int(flag.item())
                    else _scene_report(out.cpu().numpy(), n, 2))
             return (outs if is_t else [_device.to_host(o) for o in outs]), rep
+    if not is_t and not any(isinstance(b, torch.Tensor) for b in bands):
+        # numpy in: the inputs go up once and the fused bands come down once
+        # (fuse() on the host path, then qnr() of its numpy result, would move
+        # the fused bands back up); same bits as the two separate calls
+        out_dt = _device.np_out_dtype(pan)
+        p_f = _device.to_device(pan, out_dt)
+        m_f = [_device.to_device(b, out_dt) for b in bands]
+        fused_t = _fusion.fuse(p_f, m_f, method)
+        p_q = p_f if p_f.dtype == (torch.float32 if _device.is_f32(pan) else torch.float64) \
+            else _plane(pan)
+        m_q = [mf if mf.dtype == (torch.float32 if _device.is_f32(b) else torch.float64)
+               else _plane(b) for mf, b in zip(m_f, bands)]
+        rep = qnr(fused_t, m_q, p_q)
+        return [_device.to_host(f) for f in fused_t], rep
     fused = _fusion.fuse(pan, ms, method)
     return fused, qnr(fused, ms, pan)

@@ -59,3 +59,6 @@ for rep in range(2):
 for rep in range(2):
     wf.resample_bilinear(ms[0], W, H)
     t = lap(f"resample_bilinear numpy 2x call {rep + 1}", t)
+for rep in range(2):
+    wf.fuse_and_qnr(pan, ms, wf.DwtReplace(wf.WaveletKind.DAUB4))
+    t = lap(f"fuse_and_qnr numpy D4 call {rep + 1}", t)
