@@ -18,6 +18,9 @@ import torch
 from . import _native
 
 _UPLOAD_MIN = 8 << 20  # bytes; smaller planes go through torch's copy
+# PAN rows per host-pipeline strip (0 = the library default); WF_HOST_STRIP_ROWS
+# overrides (each of the 3 slots pins (4 + 5 B) x rows x W bytes of staging)
+_HOST_STRIP_ROWS = int(__import__("os").environ.get("WF_HOST_STRIP_ROWS", "0"))
 _ctxs: list[int] = []
 _free: list[int] = []
 _ctx_lock = threading.Lock()
@@ -99,7 +102,7 @@ def host_ctx():
         ctx = _free.pop() if _free else None
     if ctx is None:
         dev = require_cuda()
-        ctx = _native.load().wf_ctx_create(dev.index, 0)
+        ctx = _native.load().wf_ctx_create(dev.index, _HOST_STRIP_ROWS)
         if not ctx:
             _native.check(5)
         with _ctx_lock:
