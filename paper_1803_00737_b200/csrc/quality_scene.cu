@@ -695,7 +695,7 @@ constexpr int kQ2Msw = 96;               // staged MS segment: 80 cols + halo, o
 constexpr int kQ2Cons = 3 * kQ2Bc;       // consumer warps
 constexpr int kQ2Prod = 1;               // producer warps
 constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
-constexpr int kQ2TrRows = 16;            // transpose chunk (rows of 32 lanes)
+constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes): 24 -> 2.04 ms, 16 -> 2.11, 8 -> 2.37, 32 -> 2.11
 
 #ifndef WF_QNR_F64CELL  // ERGAS 2x2 sums in float64 (1) or FP32 TwoSums (0)
 #define WF_QNR_F64CELL 1
