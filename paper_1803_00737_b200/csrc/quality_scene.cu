@@ -695,12 +695,12 @@ constexpr int kQ2Msw = 96;               // staged MS segment: 80 cols + halo, o
 constexpr int kQ2Cons = 3 * kQ2Bc;       // consumer warps
 constexpr int kQ2Prod = 1;               // producer warps
 constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
-constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes): 24 -> 2.04 ms, 16 -> 2.11, 8 -> 2.37, 32 -> 2.11
+constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes) when WF_Q2_SHFL=0: 24 -> 2.04 ms, 16 -> 2.11, 8 -> 2.37, 32 -> 2.11
 
 #ifndef WF_QNR_F64CELL  // ERGAS 2x2 sums in float64 (1) or FP32 TwoSums (0)
 #define WF_QNR_F64CELL 1
 #endif
-#ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound)
+#ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound); 2 -> 2.24 ms, 3 -> 2.03, 4 -> 2.33
 #define WF_Q2_STAGES 3
 #endif
 // Tensor maps of the scene planes (2-D, float32): the producer moves a
@@ -760,9 +760,45 @@ __device__ __forceinline__ void q2_flush(float* tr, int n, double* ds, int lane)
 
 // Transpose-and-sum NR per-lane values v[0..NR) into ds[idx(r)] (float64),
 // in chunks of kQ2TrRows rows through the warp's buffer.
+#ifndef WF_Q2_SHFL  // per-tile lane sums by shuffle butterfly (1) or smem transpose (0)
+#define WF_Q2_SHFL 1
+#endif
 template <int NR, typename Idx>
 __device__ __forceinline__ void q2_reduce(float* tr, double* ds, int lane, const float (&v)[NR],
                                           Idx idx) {
+#if WF_Q2_SHFL
+  // Butterfly over lane offsets 16, 8, 4, 1, 2: each add pairs the same two
+  // partials as lane_sum32's tree (lanes j / j+16, then +8, +4, then the
+  // float4 x+y / z+w, then the two halves), so the sums are bit-identical to
+  // the transpose path -- without its shared-memory buffer.
+  (void)tr;
+#pragma unroll
+  for (int c0 = 0; c0 < NR; c0 += 32) {
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = c0 + i < NR ? v[c0 + i] : 0.f;
+    constexpr int kOff[5] = {16, 8, 4, 1, 2};
+    int done = 0;
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const int o = kOff[st];
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if ((i & (done | o)) == 0 && c0 + i < NR) {
+          // slot i now stands for "index i with this lane's bits"; both
+          // members of the pair past NR are zero and skipped above
+          const float a = x[i], b = c0 + (i | o) < NR ? x[i | o] : 0.f;
+          const float send = up ? a : b, keep = up ? b : a;
+          x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      done |= o;
+    }
+    // lane l holds the lane sum of value c0 + l
+    if (c0 + lane < NR) ds[idx(c0 + lane)] = (double)x[0];
+  }
+  __syncwarp();
+#else
 #pragma unroll
   for (int c0 = 0; c0 < NR; c0 += kQ2TrRows) {
     constexpr int kRows = kQ2TrRows;
@@ -774,6 +810,7 @@ __device__ __forceinline__ void q2_reduce(float* tr, double* ds, int lane, const
     for (int w = lane; w < n; w += 32) ds[idx(c0 + w)] = (double)lane_sum32(tr + w * kTrPad);
     __syncwarp();
   }
+#endif
 }
 
 template <int NB, bool FUSE>
@@ -1455,7 +1492,7 @@ static size_t q2_smem() {
   using C = Q2Cfg<NB, FUSE>;
   return 128 + (size_t)C::S * C::SLOT * sizeof(float) + C::NBAR * sizeof(uint64_t) +
          (size_t)2 * kQ2Bc * C::DS * sizeof(double) +
-         (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float) + 16;
+         (WF_Q2_SHFL ? 0 : (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float)) + 16;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
