@@ -700,6 +700,19 @@ constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes) wh
 #ifndef WF_QNR_F64CELL  // ERGAS 2x2 sums in float64 (1) or FP32 TwoSums (0)
 #define WF_QNR_F64CELL 1
 #endif
+// back-off (ns) between full-barrier probes of the F / U / L role warps (0:
+// the plain suspend-hint wait); the F role runs ahead of the other two.
+// F 200 ns: 2.035 -> 2.015 ms; F 800 ns: 2.014 (slower on small scenes);
+// F 400 + U/L 100: 2.043 (profiles/r01_qnr_backoff.log)
+#ifndef WF_Q2_FBACKOFF
+#define WF_Q2_FBACKOFF 200
+#endif
+#ifndef WF_Q2_UBACKOFF
+#define WF_Q2_UBACKOFF 0
+#endif
+#ifndef WF_Q2_LBACKOFF
+#define WF_Q2_LBACKOFF 0
+#endif
 #ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound); 2 -> 2.24 ms, 3 -> 2.03, 4 -> 2.33
 #define WF_Q2_STAGES 3
 #endif
@@ -962,7 +975,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int i = 0; i < C::ND; ++i) fd[i] = 0.f;
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
-        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
+        tma::mbar_wait_backoff<WF_Q2_FBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll
         for (int h = 0; h < C::PAIRS; ++h) {  // row pair h of the stage
@@ -1103,7 +1116,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int i = 0; i < C::ND; ++i) ud[i] = 0.f;
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
-        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
+        tma::mbar_wait_backoff<WF_Q2_UBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
         const int rb = i0 + C::PAIRS * u - 1;  // MS row of the stage box's first row
 #pragma unroll
@@ -1265,7 +1278,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
         if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
-        tma::mbar_wait_sleep(&full[s], (g / S) & 1);
+        tma::mbar_wait_backoff<WF_Q2_LBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll
         for (int h = 0; h < C::PAIRS; ++h) {

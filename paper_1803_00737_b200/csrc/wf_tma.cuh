@@ -66,6 +66,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   } while (!done);
 }
 
+// mbar_wait_sleep with a back-off of NS nanoseconds between probes, for
+// warps known to run ahead of the barrier's phase: each probe that returns
+// early costs issue slots the slower warps of the SM could use.
+template <int NS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  if constexpr (NS <= 0) {
+    mbar_wait_sleep(bar, parity);
+  } else {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(NS);
+  }
+}
+
 // One bulk global->shared copy (UBLKCP in SASS); completion is signalled on
 // `bar` as transaction bytes. dst/src 16-byte aligned, bytes % 16 == 0.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
