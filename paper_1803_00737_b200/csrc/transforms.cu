@@ -561,10 +561,6 @@ static cudaError_t launch_exact_haar(const T* pan, long long pp, const T* const*
 // with every product and sum rounded separately (no FMA), one final cast:
 // bit-identical to the transform path.
 constexpr int kExactRows = 16;
-#ifndef WF_EXACT_AHEAD
-#define WF_EXACT_AHEAD 1
-#endif
-constexpr int kExactAhead = WF_EXACT_AHEAD;  // prefetch distance in row steps
 
 // Column sharing: a CTA of 128 threads covers 127 output coefficient columns
 // [127k, 127k + 127); thread t computes column j = 127k - 1 + t, so thread 0's

@@ -28,6 +28,9 @@ def _key(short: str) -> str:
         return "fuse_haar_b" + short.split(",")[2].strip()
     if short.startswith("fuse_d4_tma_kernel<float"):
         return "fuse_daub4_b" + short.split(",")[1].strip()
+    if short.startswith("quality_split_kernel<"):  # <NB, FUSE>: bench.py reads quality_split_kernel_6
+        nb, *fuse = [t.strip() for t in short.split("<")[1].rstrip(">").split(",")]
+        return "quality_split_kernel_" + nb + ("_fused" if fuse and fuse[0] not in ("0", "false") else "")
     if short.startswith("fuse_d4_u8x8_kernel<"):
         return "fuse_d4_u8x8_kernel_" + short.split("<")[1].split(",")[0].strip()
     return "".join(c if c.isalnum() else "_" for c in short.replace("wf::", "")).strip("_")
