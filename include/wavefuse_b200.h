@@ -81,6 +81,9 @@ const char* wf_version(void);
 const char* wf_last_error(void);
 /* Number of kernel launches this thread has issued through the library. */
 int64_t wf_launch_count(void);
+/* Re-read the WF_* tuning environment variables (read once at load time
+   otherwise; experiment knobs only, results do not depend on them). */
+int wf_tuning_reload(void);
 
 /* ---- fused hot path (device buffers) ---------------------------------- */
 int wf_fuse_dwt_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,

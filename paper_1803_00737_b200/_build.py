@@ -11,6 +11,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -27,10 +28,10 @@ FLAGS = [
     "-fmad=false",
     "-Xcompiler",
     "-fPIC",
-    "-shared",
     "-Xptxas",
     "-v",
 ]
+OBJ = PKG / "build"
 
 
 def nvcc() -> str:
@@ -53,20 +54,44 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
+    then link the shared library; the log of every step goes to build.log."""
     if not force and not stale():
         return LIB
+    OBJ.mkdir(exist_ok=True)
+    inc = ["-I", str(ROOT / "include")]
+
+    def compile_one(src: Path):
+        obj = OBJ / (src.stem + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *inc, "-c", "-o", str(obj), str(src)]
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, proc
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as pool:
+        results = list(pool.map(compile_one, srcs))
+    log_text = []
+    failed = []
+    for src, obj, cmd, proc in results:
+        log_text.append(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+        if proc.returncode != 0:
+            failed.append((src, proc.stderr))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp)]
-    cmd += [str(s) for s in sources()]
-    cmd += ["-ldl"]  # peer.cu resolves cuMemGetAddressRange from libcuda at run time
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if not failed:
+        # peer.cu resolves cuMemGetAddressRange from libcuda at run time (-ldl)
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *[str(o) for _, o, _, _ in results], "-ldl"]
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        log_text.append(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+        if proc.returncode != 0:
+            failed.append((LIB, proc.stderr))
     log = PKG / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
-    if proc.returncode != 0:
-        sys.stderr.write(proc.stderr)
+    log.write_text("\n".join(log_text))
+    if failed:
+        for _, err in failed:
+            sys.stderr.write(err)
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write("\n".join(log_text))
     os.replace(tmp, LIB)
     return LIB
 

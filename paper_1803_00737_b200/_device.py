@@ -22,7 +22,7 @@ _UPLOAD_MIN = 8 << 20  # bytes; smaller planes go through torch's copy
 # overrides (each of the 3 slots pins (4 + 5 B) x rows x W bytes of staging)
 _HOST_STRIP_ROWS = int(__import__("os").environ.get("WF_HOST_STRIP_ROWS", "0"))
 _ctxs: list[int] = []
-_free: list[int] = []
+_free: dict[int, list[int]] = {}  # device index -> idle contexts bound to it
 _ctx_lock = threading.Lock()
 
 
@@ -98,10 +98,11 @@ def host_ctx():
     later callers -- e.g. the fresh ThreadPoolExecutor threads of the
     reference's fuse_tiled (tiling.py:185-189) -- reuse warm ones instead of
     re-allocating pinned memory."""
+    dev = require_cuda()  # the caller's current device: contexts are per device
     with _ctx_lock:
-        ctx = _free.pop() if _free else None
+        pool = _free.setdefault(dev.index, [])
+        ctx = pool.pop() if pool else None
     if ctx is None:
-        dev = require_cuda()
         ctx = _native.load().wf_ctx_create(dev.index, _HOST_STRIP_ROWS)
         if not ctx:
             _native.check(5)
@@ -111,7 +112,7 @@ def host_ctx():
         yield ctx
     finally:
         with _ctx_lock:
-            _free.append(ctx)
+            _free[dev.index].append(ctx)
 
 
 @atexit.register

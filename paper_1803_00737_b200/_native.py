@@ -91,6 +91,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.wf_version.restype = ctypes.c_char_p
     lib.wf_last_error.restype = ctypes.c_char_p
     lib.wf_launch_count.restype = c_i64
+    lib.wf_tuning_reload.restype = c_int
     lib.wf_ctx_create.argtypes = [c_int, c_int]
     lib.wf_ctx_create.restype = c_vp
     lib.wf_ctx_upload.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp]
@@ -148,6 +149,12 @@ def check(rc: int) -> None:
     if rc:
         msg = load().wf_last_error().decode(errors="replace")
         raise _ERR.get(rc, RuntimeError)(msg)
+
+
+def reload_tuning() -> None:
+    """Re-read the WF_* tuning environment (the library reads it once)."""
+    if _lib is not None:
+        _lib.wf_tuning_reload()
 
 
 def launch_count() -> int:

@@ -21,6 +21,38 @@
 #include "../../include/wavefuse_b200.h"
 #include "wf_kernels.h"
 
+namespace wf {
+// Environment tuning knobs, read once (the first call) instead of per call;
+// wf_tuning_reload() re-reads them (experiments and tests that change them).
+static LaunchTuning read_tuning() {
+  LaunchTuning v{};
+  auto num = [](const char* name) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : 0;
+  };
+  auto is = [](const char* name, const char* val) {
+    const char* e = getenv(name);
+    return e && strcmp(e, val) == 0;
+  };
+  v.haar_ppt = num("WF_HAAR_PPT");
+  v.d4_target_warps = num("WF_D4_TARGET_WARPS");
+  v.d4_min_pairs = num("WF_D4_MIN_PAIRS");
+  v.d4_pairs = num("WF_D4_PAIRS");
+  v.d4_stages = num("WF_D4_STAGES");
+  v.haar_u8_ppt = num("WF_HAAR_U8_PPT");
+  v.d4_u8_v1 = is("WF_D4_U8", "v1");
+  v.d4_ldg = is("WF_D4_PATH", "ldg");
+  v.no_wide = getenv("WF_NO_WIDE") != nullptr;
+  v.exact_rows = num("WF_EXACT_ROWS");
+  v.exact_transforms = getenv("WF_EXACT_TRANSFORMS") != nullptr;
+  const char* q = getenv("WF_QNR_KERNEL");
+  v.qnr_v1 = q && q[0] == 'v' && q[1] == '1';
+  return v;
+}
+static LaunchTuning g_tuning = read_tuning();
+const LaunchTuning& env_tuning() { return g_tuning; }
+}  // namespace wf
+
 namespace {
 
 thread_local std::string g_err;
@@ -112,14 +144,8 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
     vec = vec && al16(out[b]) && al16(ms[b]);
   }
 
-  wf::LaunchTuning tune{0, 0, 0, 0, 0};
-  if (const char* e = getenv("WF_HAAR_PPT")) tune.haar_ppt = atoi(e);
-  if (const char* e = getenv("WF_D4_TARGET_WARPS")) tune.d4_target_warps = atoi(e);
-  if (const char* e = getenv("WF_D4_MIN_PAIRS")) tune.d4_min_pairs = atoi(e);
-  if (const char* e = getenv("WF_D4_PAIRS")) tune.d4_pairs = atoi(e);
-  if (const char* e = getenv("WF_D4_STAGES")) tune.d4_stages = atoi(e);
-  const char* path = getenv("WF_D4_PATH");  // "ldg" forces the register-path kernel
-  const bool allow_tma = !(path && strcmp(path, "ldg") == 0);
+  const wf::LaunchTuning& tune = wf::env_tuning();
+  const bool allow_tma = !tune.d4_ldg;
   auto row16 = [](int64_t pitch) { return (pitch * (int64_t)sizeof(T)) % 16 == 0; };
 
   for (int b0 = 0; b0 < nbands; b0 += wf::kMaxBandsPerLaunch) {
@@ -153,7 +179,7 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
                             : ms[b0 + b] + (int64_t)(rows / 2 - 1) * ms_pitch;
     }
     // float64: 256-bit row accesses when every row start is 32-byte aligned
-    if (sizeof(T) == 8 && vec && !getenv("WF_NO_WIDE")) {
+    if (sizeof(T) == 8 && vec && !tune.no_wide) {
       bool w32 = al32(pan) && (pan_pitch * 8) % 32 == 0 && (out_pitch * 8) % 32 == 0;
       for (int b = 0; b < nb && w32; ++b) w32 = al32(a.out[b]);
       a.wide = w32 ? 1 : 0;
@@ -345,9 +371,54 @@ bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// Restores the calling thread's current device when a host-buffer call
+// returns (the calls switch to the context's device; the caller -- e.g. torch
+// on another GPU of the same process -- must not see that switch).
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+};
+
+// After a failed host-buffer call: wait for every copy and kernel already
+// queued on the context's streams (they may still read or write the caller's
+// buffers, which the caller frees once the error is raised) and forget the
+// pending staged outputs.
+void quiesce(wf_ctx* ctx) {
+  for (int k = 0; k < kSlots; ++k) {
+    if (ctx->slot[k].stream) cudaStreamSynchronize(ctx->slot[k].stream);
+    ctx->slot[k].pend_r0 = -1;
+  }
+  cudaGetLastError();
+}
+
+template <typename T>
+int fuse_host_impl(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const* out,
+                   int nbands, int h, int w);
+
 template <typename T>
 int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const* out,
               int nbands, int h, int w) {
+  DeviceGuard guard;
+  const int rc = fuse_host_impl<T>(ctx, kind, pan, ms, out, nbands, h, w);
+  if (rc != WF_OK && ctx) {
+    const std::string msg = g_err;  // quiesce must not replace the first error
+    quiesce(ctx);
+    g_err = msg;
+  }
+  return rc;
+}
+
+template <typename T>
+int fuse_host_impl(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const* out,
+                   int nbands, int h, int w) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   if (int e = check_kind(kind)) return e;
   if (nbands < 1) return fail(WF_ERR_BAND_COUNT, "need at least one band");
@@ -485,7 +556,11 @@ int fuse_host(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* const*
 
 extern "C" {
 
-const char* wf_version(void) { return "wavefuse-b200 0.1.0 (sm_100a)"; }
+const char* wf_version(void) { return "wavefuse-b200 0.2.0 (sm_100a)"; }
+int wf_tuning_reload(void) {
+  wf::g_tuning = wf::read_tuning();
+  return WF_OK;
+}
 const char* wf_last_error(void) { return g_err.c_str(); }
 int64_t wf_launch_count(void) { return g_launches; }
 
@@ -553,7 +628,31 @@ int wf_fuse_strip_exact_f64(int kind, const double* pan, int64_t pan_pitch,
 // GB/s; this path runs at the host-memcpy / PCIe rate). `after` = the stream
 // whose earlier work must complete before `dst` is written (the allocating
 // stream). Returns when the data is on the device.
+static int ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after);
+static int ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after);
+
 int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
+  DeviceGuard guard;
+  const int rc = ctx_upload(ctx, dst, src, bytes, after);
+  if (rc != WF_OK && ctx) {
+    const std::string msg = g_err;
+    quiesce(ctx);
+    g_err = msg;
+  }
+  return rc;
+}
+int wf_ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
+  DeviceGuard guard;
+  const int rc = ctx_download(ctx, dst, src, bytes, after);
+  if (rc != WF_OK && ctx) {
+    const std::string msg = g_err;
+    quiesce(ctx);
+    g_err = msg;
+  }
+  return rc;
+}
+
+static int ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(WF_ERR_VALUE, "bad upload arguments");
   if (bytes == 0) return WF_OK;
@@ -598,7 +697,7 @@ int wf_ctx_upload(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* 
 // Device -> host counterpart: up to kSlots 32 MiB DMAs in flight into the
 // pinned staging while the copy workers move finished chunks to `dst`.
 // `after` = the stream that produced src. Synchronous.
-int wf_ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
+static int ctx_download(wf_ctx* ctx, void* dst, const void* src, int64_t bytes, void* after) {
   if (!ctx) return fail(WF_ERR_VALUE, "null context");
   if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(WF_ERR_VALUE, "bad download arguments");
   if (bytes == 0) return WF_OK;
@@ -651,6 +750,7 @@ int wf_ctx_set_exact(wf_ctx* ctx, int exact) {
 }
 
 wf_ctx* wf_ctx_create(int device, int strip_rows) {
+  DeviceGuard guard;
   if (cudaError_t e = cudaSetDevice(device)) {
     cuda_status(e, "cudaSetDevice");
     return nullptr;
@@ -674,6 +774,7 @@ wf_ctx* wf_ctx_create(int device, int strip_rows) {
 
 void wf_ctx_destroy(wf_ctx* c) {
   if (!c) return;
+  DeviceGuard guard;
   cudaSetDevice(c->device);
   for (int k = 0; k < kSlots; ++k) {
     if (c->slot[k].stream) {

@@ -344,6 +344,28 @@ __global__ void __launch_bounds__(kHaarThreads)
 // ---------------------------------------------------------------------------
 // Host-side launchers
 // ---------------------------------------------------------------------------
+// The Haar grids map row pairs to gridDim.y (at most 65535): taller planes
+// (H >= 131072 at one pair per thread) are launched in row chunks. Haar is
+// 2x2-local, so a chunk is an independent sub-plane at an even row offset.
+template <typename T, typename F>
+static cudaError_t haar_row_chunks(const FuseArgs<T>& a, int pairs_per_y, F&& launch) {
+  const long long npairs = a.rows >> 1;
+  const long long chunk = 65535LL * pairs_per_y;
+  for (long long p0 = 0; p0 < npairs; p0 += chunk) {
+    FuseArgs<T> c = a;
+    const long long n = npairs - p0 < chunk ? npairs - p0 : chunk;
+    c.pan = a.pan + 2 * p0 * a.pan_pitch;
+    for (int b = 0; b < a.nbands; ++b) {
+      c.ms[b] = a.ms[b] + p0 * a.ms_pitch;
+      c.out[b] = a.out[b] + 2 * p0 * a.out_pitch;
+    }
+    c.rows = (int)(2 * n);
+    launch(c);
+    if (cudaError_t e = cudaGetLastError()) return e;
+  }
+  return cudaSuccess;
+}
+
 template <typename T, typename Acc, int NB>
 static cudaError_t launch_nb(int kind, const FuseArgs<T>& a0, bool vec, cudaStream_t s,
                              const LaunchTuning& tune) {
@@ -351,21 +373,23 @@ static cudaError_t launch_nb(int kind, const FuseArgs<T>& a0, bool vec, cudaStre
   const int npairs = a.rows >> 1;
   if (kind == kHaar) {
     const int nq = (a.W + 3) / 4;
-    const int ppt = tune.haar_ppt > 0 ? tune.haar_ppt : kHaarPairsPerThread;
-    dim3 grid((nq + kHaarThreads - 1) / kHaarThreads, (npairs + ppt - 1) / ppt);
+    int ppt = tune.haar_ppt > 0 ? tune.haar_ppt : kHaarPairsPerThread;
+    if (ppt != 1 && ppt != 2 && ppt != 8) ppt = 4;
+    return haar_row_chunks(a, ppt, [&](const FuseArgs<T>& c) {
+      dim3 grid((nq + kHaarThreads - 1) / kHaarThreads, ((c.rows >> 1) + ppt - 1) / ppt);
 #define WF_HAAR_LAUNCH(P)                                                        \
   if (vec)                                                                      \
-    fuse_haar_kernel<T, Acc, NB, true, P><<<grid, kHaarThreads, 0, s>>>(a);     \
+    fuse_haar_kernel<T, Acc, NB, true, P><<<grid, kHaarThreads, 0, s>>>(c);     \
   else                                                                          \
-    fuse_haar_kernel<T, Acc, NB, false, P><<<grid, kHaarThreads, 0, s>>>(a);
-    switch (ppt) {
-      case 1: WF_HAAR_LAUNCH(1) break;
-      case 2: WF_HAAR_LAUNCH(2) break;
-      case 8: WF_HAAR_LAUNCH(8) break;
-      default: WF_HAAR_LAUNCH(4) break;
-    }
+    fuse_haar_kernel<T, Acc, NB, false, P><<<grid, kHaarThreads, 0, s>>>(c);
+      switch (ppt) {
+        case 1: WF_HAAR_LAUNCH(1) break;
+        case 2: WF_HAAR_LAUNCH(2) break;
+        case 8: WF_HAAR_LAUNCH(8) break;
+        default: WF_HAAR_LAUNCH(4) break;
+      }
 #undef WF_HAAR_LAUNCH
-    return cudaGetLastError();
+    });
   }
   // D4: choose the row-run length so that the task count fills the chip
   a.n_colbands = (a.W + kColsPerWarp - 1) / kColsPerWarp;
@@ -504,22 +528,23 @@ __global__ void __launch_bounds__(kHaarThreads)
 }
 
 template <int NB>
-static cudaError_t launch_haar_u8(const FuseArgs<uint8_t>& a, cudaStream_t s) {
+static cudaError_t launch_haar_u8(const FuseArgs<uint8_t>& a, cudaStream_t s, int ppt_tune) {
   const int ng = (a.W + 15) / 16;
-  int ppt = kHaarU8PairsPerThread;
-  if (const char* e = getenv("WF_HAAR_U8_PPT")) ppt = atoi(e) > 0 ? atoi(e) : ppt;
-  auto go = [&](auto P) {
-    constexpr int kP = decltype(P)::value;
-    dim3 grid((ng + kHaarThreads - 1) / kHaarThreads, ((a.rows >> 1) + kP - 1) / kP);
-    fuse_haar_u8_kernel<NB, kP><<<grid, kHaarThreads, 0, s>>>(a);
-  };
-  switch (ppt) {
-    case 1: go(std::integral_constant<int, 1>{}); break;
-    case 2: go(std::integral_constant<int, 2>{}); break;
-    case 8: go(std::integral_constant<int, 8>{}); break;
-    default: go(std::integral_constant<int, 4>{}); break;
-  }
-  return cudaGetLastError();
+  int ppt = ppt_tune > 0 ? ppt_tune : kHaarU8PairsPerThread;
+  if (ppt != 1 && ppt != 2 && ppt != 8) ppt = 4;
+  return haar_row_chunks(a, ppt, [&](const FuseArgs<uint8_t>& c) {
+    auto go = [&](auto P) {
+      constexpr int kP = decltype(P)::value;
+      dim3 grid((ng + kHaarThreads - 1) / kHaarThreads, ((c.rows >> 1) + kP - 1) / kP);
+      fuse_haar_u8_kernel<NB, kP><<<grid, kHaarThreads, 0, s>>>(c);
+    };
+    switch (ppt) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 8: go(std::integral_constant<int, 8>{}); break;
+      default: go(std::integral_constant<int, 4>{}); break;
+    }
+  });
 }
 
 // uint8 specialisation: Haar needs 16-byte rows (vec), D4 the bulk-copy
@@ -530,14 +555,14 @@ cudaError_t launch_fuse<uint8_t, float>(int kind, const FuseArgs<uint8_t>& a, bo
   if (kind == kDaub4) return tma ? launch_fuse_d4_tma<uint8_t>(a, s, tune) : cudaErrorInvalidValue;
   if (!vec) return cudaErrorInvalidValue;
   switch (a.nbands) {
-    case 1: return launch_haar_u8<1>(a, s);
-    case 2: return launch_haar_u8<2>(a, s);
-    case 3: return launch_haar_u8<3>(a, s);
-    case 4: return launch_haar_u8<4>(a, s);
-    case 5: return launch_haar_u8<5>(a, s);
-    case 6: return launch_haar_u8<6>(a, s);
-    case 7: return launch_haar_u8<7>(a, s);
-    case 8: return launch_haar_u8<8>(a, s);
+    case 1: return launch_haar_u8<1>(a, s, tune.haar_u8_ppt);
+    case 2: return launch_haar_u8<2>(a, s, tune.haar_u8_ppt);
+    case 3: return launch_haar_u8<3>(a, s, tune.haar_u8_ppt);
+    case 4: return launch_haar_u8<4>(a, s, tune.haar_u8_ppt);
+    case 5: return launch_haar_u8<5>(a, s, tune.haar_u8_ppt);
+    case 6: return launch_haar_u8<6>(a, s, tune.haar_u8_ppt);
+    case 7: return launch_haar_u8<7>(a, s, tune.haar_u8_ppt);
+    case 8: return launch_haar_u8<8>(a, s, tune.haar_u8_ppt);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -644,8 +644,7 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
 template <typename T>
 cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune) {
   if constexpr (sizeof(T) == 1) {
-    const char* v = getenv("WF_D4_U8");  // "v1": the 4-column kernel below
-    if (!(v && strcmp(v, "v1") == 0)) return launch_u8x8(a, s, tune);
+    if (!tune.d4_u8_v1) return launch_u8x8(a, s, tune);  // WF_D4_U8=v1: the 4-column kernel
   }
   switch (a.nbands) {
     case 1: return launch_tma_nb<T, 1, 4>(a, s, tune);

@@ -1494,10 +1494,7 @@ static size_t qs_smem() {
 
 // Which scene kernel runs: the role-split one (default) or, with
 // WF_QNR_KERNEL=v1, the one-warp-per-block one (kept for A/B timing).
-static bool qs_use_v1() {
-  const char* e = getenv("WF_QNR_KERNEL");
-  return e && e[0] == 'v' && e[1] == '1';
-}
+static bool qs_use_v1() { return env_tuning().qnr_v1 != 0; }
 
 template <int NB, bool FUSE>
 static size_t q2_smem() {

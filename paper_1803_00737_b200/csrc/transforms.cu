@@ -713,7 +713,7 @@ static cudaError_t launch_exact_d4(const T* pan, long long pp, const T* pan_top,
                                   long long mp, T* const* out, long long op, int nbands, int h,
                                   int w, cudaStream_t s) {
   int rows = kExactRows;
-  if (const char* e = getenv("WF_EXACT_ROWS")) rows = atoi(e) > 0 ? atoi(e) : rows;
+  if (env_tuning().exact_rows > 0) rows = env_tuning().exact_rows;
   dim3 grid(((w >> 1) + kExCols - 1) / kExCols, ((h >> 1) + rows - 1) / rows);
   for (int b0 = 0; b0 < nbands; b0 += kMaxBandsPerLaunch) {
     const int nb = min(kMaxBandsPerLaunch, nbands - b0);
@@ -797,7 +797,7 @@ template <typename T>
 cudaError_t launch_fuse_bands_exact(int kind, const T* pan, long long pp, const T* const* ms,
                                     long long mp, T* const* out, long long op, int nbands,
                                     int h, int w, double* ws, cudaStream_t s) {
-  if (!getenv("WF_EXACT_TRANSFORMS"))  // one pass, no coefficient image
+  if (!env_tuning().exact_transforms)  // one pass, no coefficient image
     return launch_fuse_exact_strip<T>(kind, pan, pp, nullptr, nullptr, 0, ms, nullptr, mp, out,
                                       op, nbands, h, w, s);
   run_dwt2d<T, double>(kind, false, pan, pp, ws, w, h, w, s);

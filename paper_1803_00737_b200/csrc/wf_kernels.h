@@ -42,7 +42,18 @@ struct LaunchTuning {
   int d4_pairs;         // >0: fixed row pairs per warp task (overrides the above)
   int d4_stages;        // >0: shared-memory ring depth of the TMA kernel
   int haar_ppt;         // >0: Haar row pairs per thread (1, 2, 4, 8)
+  int haar_u8_ppt;      // >0: 8 bpp Haar row pairs per thread
+  int d4_u8_v1;         // 1: the 4-column 8 bpp D4 kernel instead of the 8-column one
+  int d4_ldg;           // 1: force the register-path D4 kernel (no bulk copies)
+  int no_wide;          // 1: float64 rows through 128-bit accesses, not 256-bit
+  int exact_rows;       // >0: coefficient rows per CTA of the one-pass exact D4 kernel
+  int exact_transforms; // 1: exact mode as forward + inverse transform kernels
+  int qnr_v1;           // 1: the one-warp-per-block QNR scene kernel
 };
+
+// The tuning knobs of the environment (WF_HAAR_PPT, WF_D4_*, ...), read once
+// per process (capi.cu); experiments set them before the first call.
+const LaunchTuning& env_tuning();
 
 // vec: 16-byte vector path legal; tma: the bulk-copy D4 pipeline is legal
 // (W % 8 == 0, every row 16-byte aligned).

@@ -48,6 +48,33 @@ def _exact(flag) -> bool:
     return _EXACT_DEFAULT if flag is None else bool(flag)
 
 
+# dtypes whose every value a float32 holds exactly: a band of one of these
+# enters the reference's LL replacement (fusion.py:149, band * gain in the
+# band's own precision) unchanged when cast to a float32 PAN's dtype
+_F32_EXACT = {np.dtype(t) for t in (np.float32, np.float16, np.uint8, np.int8, np.uint16,
+                                    np.int16, np.bool_)}
+_F32_EXACT_T = {torch.float32, torch.float16, torch.bfloat16, torch.uint8, torch.int8,
+                torch.int16, torch.bool}
+
+
+def _f32_exact(b) -> bool:
+    if _is_tensor(b):
+        return b.dtype in _F32_EXACT_T
+    return np.asarray(b).dtype in _F32_EXACT
+
+
+def _exact_dt(out_dt, bands):
+    """Compute dtype of the exact kernels: the PAN's, except that a float32
+    PAN with a band float32 cannot hold (float64, wide integers) runs the
+    float64 kernels on a float64 copy of the PAN -- the reference keeps such
+    a band's full precision in the LL quadrant (fusion.py:148-150) and casts
+    only the result to float32, and so does the caller of this (one final
+    rounding, the same as astype(float32))."""
+    if out_dt == np.float32 and not all(_f32_exact(b) for b in bands):
+        return np.float64
+    return out_dt
+
+
 @dataclass(frozen=True)
 class DwtReplace:
     """fusion.py:35-40: swap the approximation quadrant of the PAN transform
@@ -204,11 +231,14 @@ def fuse_dwt(pan, ms_band, kind: WaveletKind, *, exact: bool | None = None):
     h, w = _validate_pair(_shape(pan), _shape(ms_band))
     _check_min(h, w, kind)
     out_dt = _device.np_out_dtype(pan)
-    if exact and _is_tensor(pan):
-        return _fuse_exact_device(_device.to_device(pan, out_dt),
-                                  [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
     if exact:
-        return _fuse_host(pan, [np.asarray(ms_band)], kind, out_dt, exact=True)[0]
+        cdt = _exact_dt(out_dt, [ms_band])
+        if _is_tensor(pan):
+            out = _fuse_exact_device(_device.to_device(pan, cdt),
+                                     [_device.to_device(ms_band, cdt)], kind, cdt)[0]
+            return out if cdt == out_dt else out.to(_device.torch_dtype(out_dt))
+        out = _fuse_host(pan, [np.asarray(ms_band)], kind, cdt, exact=True)[0]
+        return out if cdt == out_dt else out.astype(out_dt)
     if _is_tensor(pan):
         pan_t = _device.to_device(pan, out_dt)
         return _fuse_device(pan_t, [_device.to_device(ms_band, out_dt)], kind, out_dt)[0]
@@ -248,14 +278,19 @@ def fuse(pan, ms, method: FusionMethod, *, exact: bool | None = None):
         _validate_pair(shape, _shape(b))
     _check_min(h, w, method.kind)
     out_dt = _device.np_out_dtype(pan)
-    if exact and (_is_tensor(pan) or any(_is_tensor(b) for b in resampled)):
-        outs = _fuse_exact_device(_device.to_device(pan, out_dt),
-                                  [_device.to_device(b, out_dt) for b in resampled],
-                                  method.kind, out_dt)
-        return outs if _is_tensor(pan) else [_device.to_host(o) for o in outs]
-    if exact:  # host buffers: the strip pipeline with the exact kernels
-        return _fuse_host(pan, [np.asarray(b) for b in resampled], method.kind, out_dt,
-                          exact=True)
+    if exact:
+        cdt = _exact_dt(out_dt, resampled)
+        cast = (lambda o: o) if cdt == out_dt else (
+            lambda o: o.to(_device.torch_dtype(out_dt)) if _is_tensor(o) else o.astype(out_dt))
+        if _is_tensor(pan) or any(_is_tensor(b) for b in resampled):
+            outs = _fuse_exact_device(_device.to_device(pan, cdt),
+                                      [_device.to_device(b, cdt) for b in resampled],
+                                      method.kind, cdt)
+            outs = [cast(o) for o in outs]
+            return outs if _is_tensor(pan) else [_device.to_host(o) for o in outs]
+        # host buffers: the strip pipeline with the exact kernels
+        return [cast(o) for o in _fuse_host(pan, [np.asarray(b) for b in resampled],
+                                            method.kind, cdt, exact=True)]
     if _is_tensor(pan) or any(_is_tensor(b) for b in resampled):
         pan_t = _device.to_device(pan, out_dt)
         bands_t = [_device.to_device(b, out_dt) for b in resampled]

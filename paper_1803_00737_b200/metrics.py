@@ -447,7 +447,9 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
             and all(_shape(b) == (p_shape[0] // 2, p_shape[1] // 2) for b in bands)
             and p_shape[0] % 2 == 0 and p_shape[1] % 2 == 0)
     if fast:
-        p_t = _device.to_device(pan, np.float32) if (is_t or _device.is_f32(pan)) else None
+        # only a genuinely float32 PAN qualifies: a float64 / integer PAN fuses to
+        # float64 (fusion.py:46-47), which this float32 kernel does not produce
+        p_t = _device.to_device(pan, np.float32) if _device.is_f32(pan) else None
         m_t = [_plane(b) for b in bands] if p_t is not None else []
         n = len(m_t)
         h, w = p_shape

@@ -26,6 +26,7 @@ from .fusion import (
     DwtReplace,
     FusionMethod,
     _exact,
+    _exact_dt,
     _quantize_dev,
     _u8_device,
     _u8_to_f32_dev,
@@ -197,9 +198,12 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
         # wire_planes: bands to half size (bilinear), then everything to uint8
         low = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0]) for b in bands]
 
-        def to_u8(x):  # uint8 passes through; float planes are quantised (float32)
+        def to_u8(x):  # uint8 passes through; other planes are quantised in their
+            # own dtype rule (float32 iff float32, else float64), like the
+            # reference's quantize on the numpy plane (imageio.py:115-123)
             is_u8 = x.dtype == (torch.uint8 if isinstance(x, torch.Tensor) else np.uint8)
-            return _u8_device(x) if is_u8 else _quantize_dev(_device.to_device(x, np.float32))
+            return _u8_device(x) if is_u8 else _quantize_dev(
+                _device.to_device(x, _device.np_out_dtype(x)))
 
         pan_u8 = to_u8(pan)
         ms_u8 = [to_u8(b) for b in low]
@@ -214,11 +218,16 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
             outs = [_quantize_dev(f) for f in fo]
         return outs if is_t else [_device.to_host(o) for o in outs]
 
-    dt = _device.np_out_dtype(pan)
+    out_dt = _device.np_out_dtype(pan)
     sized = [b if _shape(b) == half else resample_bilinear(b, half[1], half[0]) for b in bands]
+    # exact: a float32 PAN with float64 bands runs the float64 kernels and
+    # casts once at the end, like the reference (fusion._exact_dt)
+    dt = _exact_dt(out_dt, sized) if exact else out_dt
     pan_t = _device.to_device(pan, dt)
     ms_t = [_device.to_device(b, dt) for b in sized]
     outs = [torch.empty_like(pan_t) for _ in ms_t]
     _window_fuse(kind, pan_t, ms_t, outs, grid, exact=exact)
+    if dt != out_dt:
+        outs = [o.to(_device.torch_dtype(out_dt)) for o in outs]
     return outs if is_t else [_device.to_host(o) for o in outs]
 

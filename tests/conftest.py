@@ -18,6 +18,17 @@ if str(ROOT) not in sys.path:
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
+@pytest.fixture(autouse=True)
+def _retune_after_env_changes():
+    """The library reads its WF_* tuning variables once; tests that
+    monkeypatch them call _native.reload_tuning(), and this fixture (set up
+    before, torn down after monkeypatch) re-reads the restored environment."""
+    yield
+    from paper_1803_00737_b200 import _native
+
+    _native.reload_tuning()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 device (sm_100a)")
 

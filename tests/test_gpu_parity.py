@@ -333,8 +333,10 @@ def test_tma_and_register_paths_bit_identical(shape, monkeypatch):
     pan = torch.rand((H, W), generator=g, device="cuda") * 255
     bands = [torch.rand((H // 2, W // 2), generator=g, device="cuda") * 255 for _ in range(B)]
     monkeypatch.delenv("WF_D4_PATH", raising=False)
+    _native.reload_tuning()
     fast = wf.fuse(pan, bands, wf.DwtReplace(KINDS["daub4"]))
     monkeypatch.setenv("WF_D4_PATH", "ldg")
+    _native.reload_tuning()
     slow = wf.fuse(pan, bands, wf.DwtReplace(KINDS["daub4"]))
     for a, b in zip(fast, slow):
         assert torch.equal(a, b)

@@ -13,6 +13,7 @@ import pytest
 import torch
 
 import paper_1803_00737_b200 as wf
+from paper_1803_00737_b200 import _native
 from oracle import cpu_dwt as O
 
 pytestmark = pytest.mark.gpu
@@ -170,6 +171,7 @@ def test_u8_d4_equals_quantized_f32_kernel(shape, nb, variant, monkeypatch):
     outside [0, 255] before the clamp."""
     if variant == "v1":
         monkeypatch.setenv("WF_D4_U8", "v1")
+        _native.reload_tuning()
     rng = np.random.default_rng(11 + nb)
     H, W = shape
     pan = rng.integers(0, 256, (H, W), dtype=np.uint8)
