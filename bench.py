@@ -12,9 +12,17 @@ multi-band kernel. Inputs are synthetic (device counter-hash uniform[0,255),
 the reference's bench draws uniform[0,255) too, bench.py:39-47) and are
 2.24 GB per scene, far larger than the 126 MB L2, so no flush is needed.
 
-N > 1 (torchrun, one process per GPU): each rank fuses its own scene (scenes
-are independent), weak scaling, no data-path collective; the
-step time is the max over ranks (NCCL all-reduce of the CUDA-event times).
+The same line carries configs[3] under "strip65536" (one 65536 x 65536 D4
+scene in row strips over the ranks, the halo exchange inside every step,
+strong scaling) and configs[4] under "batch64" (64 Landsat scenes x Haar and
+D4, each fused and QNR-scored, scenes sharded over the ranks).
+
+N > 1: one process per GPU. Under torchrun the RANK/WORLD_SIZE environment is
+used; `python bench.py --gpus N` without it re-launches itself through
+torch.distributed.run with N ranks on 127.0.0.1. Each rank fuses its own
+Landsat scene (scenes are independent), weak scaling, no
+data-path collective; the step time is the max over ranks (NCCL all-reduce
+of the CUDA-event times).
 
 metric value = whole-job PAN megapixels per second (scene-MPix/s, the
 reference's bench.py:100 unit): N * H * W * K / max_rank_time.
@@ -58,15 +66,20 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=1024,
                     help="PAN rows of the bounded CPU sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--workload", choices=["landsat", "strip65536", "batch64"], default="landsat",
+    ap.add_argument("--workload", choices=["landsat", "strip65536", "batch64", "plumbing"],
+                    default="landsat",
                     help="landsat = configs[1]/[2] (default); strip65536 = configs[3]: one "
                          "65536x65536 PAN + 1 band, D4, row strips over the ranks with the "
                          "NCCL halo exchange inside every step")
     ap.add_argument("--strip-size", type=int, default=65536)
     ap.add_argument("--scenes", type=int, default=64, help="batch64: scenes in the batch")
-    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
-                    help="strip65536: D4 halo rows read from the neighbours' HBM through CUDA "
-                         "IPC inside the kernel (peer) or exchanged by NCCL send/recv each step")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="nccl",
+                    help="C4 strips: D4 halo rows exchanged by NCCL send/recv each step (default) "
+                         "or read from the neighbours' HBM through CUDA IPC inside the kernel "
+                         "(peer; falls back to nccl without peer access)")
+    ap.add_argument("--no-subconfigs", action="store_true",
+                    help="landsat: skip the C4 (strip65536) and C5 (batch64) sub-objects")
+    ap.add_argument("--c5-steps", type=int, default=3, help="timed steps of the C5 sub-object")
     return ap.parse_args()
 
 
@@ -753,6 +766,15 @@ def run_ours(args, rank, world, local_rank):
                 "sample": (f"first {args.cpu_rows} PAN rows x {W} cols + 6 bands of the scene, "
                            f"{kname}, oracle port of the reference (numpy f64), {t:.2f} s"),
             }
+    # BASELINE configs[3] and [4] in the same run (strong scaling over the
+    # ranks): the Landsat scene's buffers go back first
+    del scene
+    torch.cuda.empty_cache()
+    c4 = c5 = None
+    if not args.no_subconfigs:
+        c4 = measure_strips(args, dist, rank, world, local_rank)
+        c5 = measure_batch(args, dist, rank, world, local_rank, max(1, args.c5_steps),
+                           min(2, max(1, args.warmup)))
     if rank == 0:
         hr = results["haar"]
         line = {
@@ -798,10 +820,18 @@ def run_ours(args, rank, world, local_rank):
                 "e2e": results["daub4"]["e2e"],
                 "cpu_baseline": cpu.get("daub4"),
             },
+            # configs[2] at the top level too (the driver parses top-level keys)
+            "value_daub4": round(results["daub4"]["value"], 3),
+            "ms_per_step_daub4": round(results["daub4"]["ms_per_step"], 4),
+            "roofline_frac_daub4": results["daub4"]["roofline"]["frac"],
+            "value_strip65536": c4["value"] if c4 else None,
+            "value_batch64": c5["value"] if c5 else None,
             "u8_8bpp": u8,
             "f64": f64,
             "exact": exact,
             "quality": quality,
+            "strip65536": c4,
+            "batch64": c5,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -809,15 +839,18 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def run_strips(args, rank, world, local_rank):
+def measure_strips(args, dist, rank, world, local_rank):
     """configs[3]: one N x N D4 scene (1 band) cut into row strips, one per
-    rank; each timed step = halo ring exchange (NCCL send/recv) + strip
-    kernel. Strong scaling: total work fixed."""
+    rank; each timed step = the halo exchange + the strip kernel. Strong
+    scaling: total work fixed. Halo transport: NCCL send/recv ring (default),
+    or --halo peer (the neighbours' rows read through CUDA IPC mappings by the
+    strip kernel; falls back to NCCL unless every rank can access its ring
+    neighbours' memory). Returns the sub-object (rank 0) or None."""
     import torch
 
     from paper_1803_00737_b200 import WaveletKind, _native, strips, synth
+    from paper_1803_00737_b200.scene import scene_bytes
 
-    dist, local_rank = init_dist(world, local_rank)
     n = args.strip_size
     r0, r1 = strips.strip_bounds(n, world, rank)
     rows = r1 - r0
@@ -830,7 +863,8 @@ def run_strips(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()  # all strips exist before neighbours map them
-    peer = strips.PeerHalos(pan, [ms]) if args.halo == "peer" else None
+    peer = strips.PeerHalos.try_create(pan, [ms]) if args.halo == "peer" else None
+    halo_mode = "peer" if peer is not None else "nccl"
 
     def step():
         halos = peer if peer is not None else strips.exchange_halos(pan, [ms])
@@ -857,79 +891,71 @@ def run_strips(args, rank, world, local_rank):
         t = torch.tensor([ms_t], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_t = float(t.item())
-    from paper_1803_00737_b200.scene import scene_bytes
-
     peak, peak_kind = peaks()
     strip_bytes = scene_bytes(rows, n, 1)
-    per_launch = ms_t / args.steps
-    achieved = strip_bytes / (per_launch * 1e-3) / 1e9
+    per_step = ms_t / args.steps
+    achieved = strip_bytes / (per_step * 1e-3) / 1e9
     if dist:
         dist.barrier()  # neighbours finished reading before the mappings go away
     if peer is not None:
         peer.close()
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(n * n * args.steps / (ms_t * 1e-3) / 1e6, 3),
-            "unit": UNIT,
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(per_launch, 4),
-            "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (device counter-hash uniform[0,255) f32)",
-            "config": {"workload": f"C4: one {n}x{n} PAN + 1 MS band, D4 periodic wrap, "
-                                   f"row strips of {rows} rows per rank",
-                       "halo": ("peer: neighbours' halo rows bulk-copied from their HBM by the "
-                                "strip kernel (CUDA IPC over NVLink), no collective per step")
-                       if args.halo == "peer" else "nccl: batched send/recv ring each step",
-                       "global_batch": 1, "parallelism": f"row strips x{world}",
-                       "l2": "no flush: inputs >> 126 MB L2"},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": peak_kind,
-                         "algorithmic_bytes_per_launch": strip_bytes,
-                         "note": "per-rank strip bytes / per-step time (halo exchange included)"},
+    del pan, ms, out
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    res = {
+        "value": round(n * n * args.steps / (ms_t * 1e-3) / 1e6, 3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(per_step, 4),
+        "scaling": "strong",
+        "workload": (f"C4: one {n}x{n} PAN + 1 MS band f32, D4 periodic wrap, row strips of "
+                     f"{rows} rows per rank (BASELINE configs[3])"),
+        "halo": ("peer: neighbours' halo rows bulk-copied from their HBM by the strip kernel "
+                 "(CUDA IPC), no collective per step") if halo_mode == "peer"
+                else "nccl: batched send/recv ring of 2+2 PAN rows + 1 MS row each step",
+        "halo_requested": args.halo,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_kind, "algorithmic_bytes_per_launch": strip_bytes,
+                     "kernel": "fuse_d4_tma_kernel<f32,B=1,4> (strip mode, halo rows)",
+                     "note": "per-rank strip bytes / per-step time (halo exchange included)"},
+    }
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        crow = 512
+        rate, t = cpu_sample_shape("daub4", crow, n, 1, threads)
+        res["cpu_baseline"] = {
+            "value": round(rate, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"first {crow} PAN rows x {n} cols + 1 band of the C4 scene, D4, oracle "
+                       f"port of the reference (numpy f64, exact row strips), {t:.2f} s; a "
+                       "per-pixel rate, so no extrapolation to the full scene"),
         }
-        if world == 1 and not args.no_cpu:
-            threads = os.cpu_count() or 1
-            rows = 512
-            rate, t = cpu_sample_shape("daub4", rows, n, 1, threads)
-            line["cpu_baseline"] = {
-                "value": round(rate, 3), "unit": "scene-MPix/s", "cores": threads, "kind": "port",
-                "sample": (f"first {rows} PAN rows x {n} cols + 1 band of the C4 scene, D4, oracle "
-                           f"port of the reference (numpy f64, exact row strips), {t:.2f} s; a "
-                           "per-pixel rate, so no extrapolation to the full scene"),
-            }
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    return res
 
 
-def run_batch(args, rank, world, local_rank):
+def measure_batch(args, dist, rank, world, local_rank, steps, warmup):
     """configs[4]: a batch of Landsat-shaped scenes partitioned by scene over
     the ranks (round-robin, no collective). Per owned scene and per wavelet a
     step runs the fused kernel and the one-pass QNR/ERGAS report on the
     result. Inputs of all owned scenes are device-resident (64 x 2.24 GB fits
-    one B200); one output set per rank is reused scene after scene."""
+    one B200); one output set per rank is reused scene after scene. Returns
+    the sub-object (rank 0) or None."""
     import torch
 
     import paper_1803_00737_b200 as wf
     from paper_1803_00737_b200 import _native, strips, synth
     from paper_1803_00737_b200.scene import DeviceScene
 
-    dist, local_rank = init_dist(world, local_rank)
     mine = strips.shard(list(range(args.scenes)), rank, world)
     scenes = []
     out = None
-    for s in mine:
-        sc = DeviceScene.synthetic(H, W, B, seed=synth.DEFAULT_SEED, scene=s)
+    for s_ in mine:
+        sc = DeviceScene.synthetic(H, W, B, seed=synth.DEFAULT_SEED, scene=s_)
         if out is None:
             out = sc.out
         else:
@@ -952,7 +978,7 @@ def run_batch(args, rank, world, local_rank):
             if record:
                 reports.append(rep.qnr)
 
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         step(False)
     torch.cuda.synchronize()
     if dist:
@@ -962,7 +988,7 @@ def run_batch(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step(True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -972,53 +998,135 @@ def run_batch(args, rank, world, local_rank):
         t = torch.tensor([ms_t], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_t = float(t.item())
+    del scenes, runs, out
+    torch.cuda.empty_cache()
     passes = len(kinds) * args.scenes  # scene-wavelet passes per step, whole job
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(passes * H * W * args.steps / (ms_t * 1e-3) / 1e6, 3),
-            "unit": "scene-MPix/s (fused + QNR report per scene and wavelet)",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(ms_t / args.steps, 3),
-            "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (device counter-hash uniform[0,255) f32, Landsat-7-shaped)",
-            "config": {"workload": f"C5: {args.scenes} Landsat-shaped scenes x (Haar, D4), "
-                                   "each fused and scored (QNR/ERGAS) on the GPU",
-                       "global_batch": args.scenes, "bands": B,
-                       "parallelism": f"scene-sharded x{world} (round-robin, no collective)",
-                       "scenes_per_rank": len(mine)},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "qnr_sample": round(float(sum(reports) / max(1, len(reports))), 6),
+    if rank != 0:
+        return None
+    res = {
+        "value": round(passes * H * W * steps / (ms_t * 1e-3) / 1e6, 3),
+        "unit": "scene-MPix/s (fused + QNR report per scene and wavelet)",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": max(1, warmup),
+        "ms_per_step": round(ms_t / steps, 3),
+        "scaling": "strong",
+        "workload": (f"C5: {args.scenes} Landsat-shaped scenes x (Haar, D4), each fused and "
+                     "scored (QNR/ERGAS) on the GPU (BASELINE configs[4])"),
+        "global_batch": args.scenes,
+        "parallelism": f"scene-sharded x{world} (round-robin, no collective)",
+        "scenes_per_rank": len(mine),
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "qnr_sample": round(float(sum(reports) / max(1, len(reports))), 6),
+    }
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        crow = 512
+        rate, t = cpu_sample_shape("haar", crow, W, B, threads, with_qnr=True)
+        res["cpu_baseline"] = {
+            "value": round(rate, 4), "unit": res["unit"], "cores": threads, "kind": "port",
+            "sample": (f"first {crow} PAN rows x {W} cols + {B} bands of one scene, Haar "
+                       f"fused (oracle port, {threads} threads) and scored (oracle qnr, one "
+                       f"thread), {t:.1f} s; per-pixel rate of one scene-wavelet pass"),
         }
-        if world == 1 and not args.no_cpu:
-            threads = os.cpu_count() or 1
-            rows = 512
-            rate, t = cpu_sample_shape("haar", rows, W, B, threads, with_qnr=True)
-            line["cpu_baseline"] = {
-                "value": round(rate, 4), "unit": line["unit"], "cores": threads, "kind": "port",
-                "sample": (f"first {rows} PAN rows x {W} cols + {B} bands of one scene, Haar "
-                           f"fused (oracle port, {threads} threads) and scored (oracle qnr, one "
-                           f"thread), {t:.1f} s; per-pixel rate of one scene-wavelet pass"),
-            }
-        print(json.dumps(line), flush=True)
+    return res
+
+
+def _standalone_line(sub, args):
+    line = {"metric": METRIC, "higher_is_better": True, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (device counter-hash uniform[0,255) f32)"}
+    line.update({k: v for k, v in sub.items() if k != "workload"})
+    line["config"] = {"workload": sub["workload"], "global_batch": sub.get("global_batch", 1),
+                      "parallelism": sub.get("parallelism", f"row strips x{sub['n_gpus']}"),
+                      "l2": "no flush: inputs >> 126 MB L2"}
+    return line
+
+
+def run_strips(args, rank, world, local_rank):
+    dist, local_rank = init_dist(world, local_rank)
+    sub = measure_strips(args, dist, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(_standalone_line(sub, args)), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
+def run_batch(args, rank, world, local_rank):
+    dist, local_rank = init_dist(world, local_rank)
+    sub = measure_batch(args, dist, rank, world, local_rank, args.steps, args.warmup)
+    if rank == 0:
+        print(json.dumps(_standalone_line(sub, args)), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_plumbing(args, rank, world):
+    """CPU-only check of the multi-process plumbing (spawn, rendezvous, barrier,
+    max-over-ranks timing, rank-0 JSON line) with gloo: no GPU work, so the
+    CPU test suite can prove `bench.py --gpus N` really starts N ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as td
+
+    if world > 1:
+        td.init_process_group("gloo")
+    a = np.random.default_rng(rank).random((256, 256))
+    for _ in range(args.warmup):
+        a = a @ a.T / 256.0
+    if world > 1:
+        td.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a = a @ a.T / 256.0
+    sec = time.perf_counter() - t0
+    ranks = torch.tensor([float(rank)])
+    t = torch.tensor([sec])
+    if world > 1:
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+        td.all_reduce(ranks, op=td.ReduceOp.SUM)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "workload": "plumbing (no GPU work)", "n_gpus": world,
+                          "world_size": world, "rank_sum": int(ranks.item()),
+                          "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(1e3 * float(t.item()) / max(1, args.steps), 4)}),
+              flush=True)
+    if world > 1:
+        td.barrier()
+        td.destroy_process_group()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun's environment: start N ranks, one
+    process per GPU, through torch.distributed.run on 127.0.0.1 (the same
+    launch the driver uses), and return their exit status. Rank 0 prints the
+    JSON line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.workload == "plumbing":
+        run_plumbing(args, rank, world)
         return
     if args.workload == "strip65536":
         run_strips(args, rank, world, local_rank)

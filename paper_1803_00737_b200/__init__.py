@@ -15,6 +15,7 @@ from .errors import (
     DimensionMismatch,
     FusionError,
     MalformedHeader,
+    MissingTile,
     NotDivisible,
     OddDimension,
     OddLength,
@@ -41,7 +42,8 @@ from .fusion import (
 from .metrics import (PendingReport, QualityReport, d_lambda, d_s, degrade, ergas, fuse_and_qnr,
                       q_index, qnr, qnr_async)
 from .pnm import PnmRaster, fuse_pnm, read_pnm, to_plane, write_pnm
-from .tiling import TileGrid, fuse_tiled, pad_edge, pad_inputs, padded_dims, plan_grid
+from .tiling import (Tile, TileGrid, fuse_tiled, merge, pad_edge, pad_inputs, padded_dims,
+                     plan_grid, split)
 from .wavelet import (
     FilterBank,
     WaveletKind,
@@ -64,12 +66,14 @@ __all__ = [
     "FusionError",
     "FusionMethod",
     "MalformedHeader",
+    "MissingTile",
     "NotDivisible",
     "OddDimension",
     "OddLength",
     "OddTile",
     "PnmRaster",
     "QualityReport",
+    "Tile",
     "TileGrid",
     "TooFewBands",
     "TooShort",
@@ -95,6 +99,7 @@ __all__ = [
     "fuse_quantized",
     "fuse_tile_quantized",
     "fuse_tiled",
+    "merge",
     "method_from_name",
     "pad_edge",
     "pad_inputs",
@@ -104,6 +109,7 @@ __all__ = [
     "qnr",
     "qnr_async",
     "set_exact_default",
+    "split",
     "PendingReport",
     "quantize",
     "read_pnm",

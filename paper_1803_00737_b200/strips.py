@@ -138,6 +138,27 @@ class PeerHalos:
         self.pan_bot = open_(nh) + no
         self.ms_top = [open_(h) + o + (prev["mrows"] - 1) * mpitch * es for h, o in prev["ms"]]
 
+    @classmethod
+    def try_create(cls, pan: torch.Tensor, ms: list[torch.Tensor], group=None):
+        """A PeerHalos mapping if every rank can read both ring neighbours'
+        memory directly (same device, or cudaDeviceCanAccessPeer over
+        NVLink), else None -- the caller then exchanges the halo rows with
+        NCCL (exchange_halos). Collective: every rank must call it."""
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if world == 1:
+            return cls(pan, ms, group)
+        dev = pan.device.index
+        devs: list = [None] * world
+        dist.all_gather_object(devs, dev, group)
+        rank = dist.get_rank(group)
+        ok = all(d == dev or torch.cuda.can_device_access_peer(dev, d)
+                 for d in (devs[(rank - 1) % world], devs[(rank + 1) % world]))
+        verdict: list = [None] * world
+        dist.all_gather_object(verdict, bool(ok), group)
+        if not all(verdict):
+            return None
+        return cls(pan, ms, group)
+
     def close(self) -> None:
         lib = _native.load()
         for b in self._opened:

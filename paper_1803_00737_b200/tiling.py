@@ -21,7 +21,8 @@ import numpy as np
 import torch
 
 from . import _device, _native
-from .errors import BandCountMismatch, DimensionMismatch, NotDivisible, OddTile, TooSmall
+from .errors import (BandCountMismatch, DimensionMismatch, MissingTile, NotDivisible, OddTile,
+                     TooSmall)
 from .fusion import (
     DwtReplace,
     FusionMethod,
@@ -69,6 +70,86 @@ def plan_grid(pan_w: int, pan_h: int, grid_w: int, grid_h: int) -> TileGrid:
     if tile_w % 2 or tile_h % 2:
         raise OddTile(f"tile {tile_w}x{tile_h} has an odd dimension")
     return TileGrid(grid_w, grid_h, tile_w, tile_h, tile_w // 2, tile_h // 2)
+
+
+@dataclass(frozen=True)
+class Tile:
+    """tiling.py Tile: grid position (row, col), the PAN crop and the
+    half-resolution band crops."""
+
+    index: tuple
+    pan: object
+    ms: list
+
+
+def _crop(plane, row: int, col: int, tile_w: int, tile_h: int):
+    """One tile of a plane as a fresh contiguous array: a device copy for a
+    CUDA tensor (the plane never leaves HBM), a host copy for numpy."""
+    piece = plane[row * tile_h:(row + 1) * tile_h, col * tile_w:(col + 1) * tile_w]
+    if isinstance(piece, torch.Tensor):
+        return piece.contiguous() if not piece.is_contiguous() else piece.clone()
+    return np.ascontiguousarray(piece)
+
+
+def split(pan, ms, grid: TileGrid) -> list:
+    """tiling.py:93-118: cut the PAN and half-resolution bands into row-major
+    contiguous tiles. Pure data movement (no arithmetic): CUDA tensors are
+    cropped on the device, numpy planes on the host, as the reference does.
+    (The fused paths never call this: fuse_tiled launches the kernels on
+    strided windows of the whole plane instead of copying tiles.)"""
+    pan_arr = pan if isinstance(pan, torch.Tensor) else np.asarray(pan)
+    bands = [b if isinstance(b, torch.Tensor) else np.asarray(b) for b in ms]
+    if _shape(pan_arr) != (grid.pan_h, grid.pan_w):
+        raise DimensionMismatch(
+            f"panchromatic {_shape(pan_arr)} does not match grid {grid.pan_w}x{grid.pan_h}")
+    half = (grid.pan_h // 2, grid.pan_w // 2)
+    for b in bands:
+        if _shape(b) != half:
+            raise DimensionMismatch(f"band {_shape(b)} is not half-size {half}")
+    tiles = []
+    for row in range(grid.grid_h):
+        for col in range(grid.grid_w):
+            tiles.append(Tile((row, col),
+                              _crop(pan_arr, row, col, grid.pan_tile_w, grid.pan_tile_h),
+                              [_crop(b, row, col, grid.ms_tile_w, grid.ms_tile_h)
+                               for b in bands]))
+    return tiles
+
+
+def merge(tiles, grid: TileGrid) -> list:
+    """tiling.py:121-152: assemble per-tile fused bands (row-major order)
+    into full planes, placed by list index, never by arrival order. Device
+    tiles are assembled in HBM (tensor out), host tiles on the host."""
+    tiles = list(tiles)
+    if len(tiles) != grid.tile_count:
+        raise MissingTile(f"got {len(tiles)} tiles, grid has {grid.tile_count}")
+    for i, t in enumerate(tiles):
+        if t is None:
+            raise MissingTile(f"tile index {i} is absent")
+    first = tiles[0]
+    band_count = len(first)
+    th, tw = grid.pan_tile_h, grid.pan_tile_w
+    for t in tiles:
+        if len(t) != band_count:
+            raise DimensionMismatch(f"band counts differ: {len(t)} vs {band_count}")
+        for b in t:
+            if _shape(b) != (th, tw):
+                raise DimensionMismatch(f"tile band {_shape(b)} is not {tw}x{th}")
+    on_dev = isinstance(first[0], torch.Tensor)
+    if on_dev:
+        out = [torch.empty((grid.pan_h, grid.pan_w), dtype=first[k].dtype,
+                           device=first[k].device) for k in range(band_count)]
+    else:
+        out = [np.empty((grid.pan_h, grid.pan_w), dtype=np.asarray(first[k]).dtype)
+               for k in range(band_count)]
+    for i, t in enumerate(tiles):
+        row, col = divmod(i, grid.grid_w)
+        for k in range(band_count):
+            src = t[k]
+            if on_dev and not isinstance(src, torch.Tensor):
+                src = torch.as_tensor(np.asarray(src), device=out[k].device)
+            out[k][row * th:(row + 1) * th, col * tw:(col + 1) * tw] = src
+    return out
 
 
 def padded_dims(w: int, h: int, grid_w: int, grid_h: int) -> tuple[int, int]:
