@@ -40,7 +40,12 @@ static LaunchTuning read_tuning() {
   v.d4_pairs = num("WF_D4_PAIRS");
   v.d4_stages = num("WF_D4_STAGES");
   v.haar_u8_ppt = num("WF_HAAR_U8_PPT");
-  v.d4_u8_v1 = is("WF_D4_U8", "v1");
+  v.d4_u8_variant = is("WF_D4_U8", "v1") ? 1 : is("WF_D4_U8", "v2") ? 2 : 0;
+  v.u8_fix_mode = is("WF_U8_FIX", "all")       ? 1
+                  : is("WF_U8_FIX", "ref")     ? 2
+                  : is("WF_U8_FIX", "skipfix") ? 3   // timing experiments only:
+                  : is("WF_U8_FIX", "nodetect") ? 4  // bytes not exact
+                                                : 0;
   v.d4_ldg = is("WF_D4_PATH", "ldg");
   v.no_wide = getenv("WF_NO_WIDE") != nullptr;
   v.exact_rows = num("WF_EXACT_ROWS");

@@ -25,6 +25,7 @@
 // Bytes in flight live in shared memory, not in registers, so a handful of
 // warps per SM keep >100 KB of HBM reads outstanding.
 #include "wf_common.cuh"
+#include "wf_exact.cuh"
 #include "wf_kernels.h"
 #include "wf_tma.cuh"
 
@@ -395,7 +396,222 @@ __device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, boo
       : "memory");
 }
 
-template <int NB, int NCW, int MINB, int CVT>
+// ---------------------------------------------------------------------------
+// Byte-exact 8 bpp D4 (v3, the default). The reference's worker computes
+// quantize(float32(float64 sequence)) (tiling.py:163-172, imageio.py:115-123);
+// the kernel computes o = pan + S_LL(2 ms - LL(pan)) in float32 with a proven
+// error bound (tools/u8_error_bound.py: 7.1e-4 including the reference's own
+// cast), adds 0.5 + 2^-9 and rounds DOWN onto a 2^-8 grid with one magic add:
+//   r = (o + 0.5 + 2^-9) + 49152  (FADD2.RM; 49152 = 1.5 * 2^15, ulp 2^-8)
+//   bits(r) = 0x47400000 + F,  F = floor(256 (o + 0.5 + 2^-9))
+// so bytes 1-2 of r hold 0x4000 + floor(o + 0.5 + 2^-9) -- clamped to the byte
+// by one VIADDMNMX.S16x2.RELU per two pixels -- and byte 0 holds the eight
+// fraction bits. A pixel whose fraction byte is 0 lies within 2^-9 of a
+// rounding boundary k + 0.5 (2.7x the error bound): only there can the
+// reference's byte differ. Such pixels are detected two per instruction
+// (PRMT the fraction byte above the low integer byte; the 16-bit lane is then
+// < 256 exactly when the fraction byte is 0; VIMNMX3.U16x2 keeps the minimum),
+// and the thread's 2 x 8-pixel unit of that band is queued in a per-warp
+// shared-memory list (0.4% of pixels, ~6% of units). At the end of its row
+// run a warp recomputes them -- one unit per lane, PAN/MS re-read through L2
+// (the CTA just bulk-copied them) -- in float64 (fix_unit_u8), and rewrites their
+// 16 bytes: a float64 value further than 1e-9 from every byte boundary of
+// the float32 cast gives the reference's byte outright (float64 evaluation
+// orders differ by << 1e-9 here); a closer one is recomputed in the
+// reference's own float64 operation order (ref_pixel_u8). The other 99.6% of
+// pixels keep the float32 byte, which is provably the reference's.
+// ---------------------------------------------------------------------------
+// queued units per warp and task: 16 row pairs x 32 lanes x NB bands x ~6% flagged
+// = ~184 expected at 6 bands; an overflow re-does the warp's whole run
+constexpr int kU8FixCap = 512;
+
+__device__ __forceinline__ uint32_t quantize_ref(float f) {  // imageio.py:115-123 in float32
+  const float c = fminf(fmaxf(f, 0.0f), 255.0f);
+  return (uint32_t)floorf(__fadd_rn(c, 0.5f));
+}
+
+// One band of an 8 bpp launch as the fix-up sees it (passed by value: a
+// reference to the kernel's FuseArgs would copy the parameter block to local
+// memory in every thread).
+struct U8Band {
+  const uint8_t* pan;
+  const uint8_t* pan_top;  // 2 halo rows above / below the launch's rows
+  const uint8_t* pan_bot;
+  const uint8_t* ms;
+  const uint8_t* ms_top;  // MS row above the launch's first row
+  uint8_t* out;
+  long long pan_pitch, halo_pitch, ms_pitch, out_pitch;
+  int rows, W, fix_mode;
+  // PAN row r of the launch (r in [-2, rows + 1]) and MS row m (m >= -1)
+  __device__ __forceinline__ const uint8_t* pan_row(int r) const {
+    if (r < 0) return pan_top + (long long)(r + 2) * halo_pitch;
+    if (r >= rows) return pan_bot + (long long)(r - rows) * halo_pitch;
+    return pan + (long long)r * pan_pitch;
+  }
+  __device__ __forceinline__ const uint8_t* ms_row(int m) const {
+    return m < 0 ? ms_top : ms + (long long)m * ms_pitch;
+  }
+};
+
+template <int NB>
+__device__ __forceinline__ U8Band u8_band(const FuseArgs<uint8_t>& a, int b) {
+  U8Band u;
+  u.ms = a.ms[0];
+  u.ms_top = a.ms_top[0];
+  u.out = a.out[0];
+#pragma unroll
+  for (int k = 1; k < NB; ++k)  // static indexing keeps the tables in the param bank
+    if (b == k) {
+      u.ms = a.ms[k];
+      u.ms_top = a.ms_top[k];
+      u.out = a.out[k];
+    }
+  u.pan = a.pan;
+  u.pan_top = a.pan_top;
+  u.pan_bot = a.pan_bot;
+  u.pan_pitch = a.pan_pitch;
+  u.halo_pitch = a.halo_pitch;
+  u.ms_pitch = a.ms_pitch;
+  u.out_pitch = a.out_pitch;
+  u.rows = a.rows;
+  u.W = a.W;
+  u.fix_mode = a.fix_mode;
+  return u;
+}
+
+// One output pixel (row y of the launch, column x) in the reference's own
+// float64 sequence (wavelet.py:73-164, fusion.py:148-150): the row pass,
+// column pass, LL <- band * 2, column inverse and row inverse of exactly the
+// coefficients this pixel depends on, periodic wrap over the window's width
+// and (through the halo rows) the scene's height; then the cast to float32
+// and quantize.
+__device__ __noinline__ uint32_t ref_pixel_u8(const U8Band u, int y, int x) {
+  const D4 t = d4_taps();
+  const int W = u.W, Wh = W >> 1;
+  const int i = y >> 1, p = y & 1, jj = x >> 1, q = x & 1;
+  double s_lo[2], s_hi[2];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {  // coefficient columns jj-1, jj
+    const int cc = side == 0 ? wrap(jj - 1, Wh) : jj;
+    double ll[2], lh[2], hl[2], hh[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // coefficient rows i-1, i
+      const int ci = i - 1 + k;
+      double rlo[4], rhi[4];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const uint8_t* row = u.pan_row(2 * ci + rr);
+        const double x0 = row[2 * cc], x1 = row[2 * cc + 1];
+        const double x2 = row[wrap(2 * cc + 2, W)], x3 = row[wrap(2 * cc + 3, W)];
+        rlo[rr] = fwd_lo(kDaub4, t, x0, x1, x2, x3);
+        rhi[rr] = fwd_hi(kDaub4, t, x0, x1, x2, x3);
+      }
+      ll[k] = mul((double)u.ms_row(ci)[cc], 2.0);
+      lh[k] = fwd_hi(kDaub4, t, rlo[0], rlo[1], rlo[2], rlo[3]);
+      hl[k] = fwd_lo(kDaub4, t, rhi[0], rhi[1], rhi[2], rhi[3]);
+      hh[k] = fwd_hi(kDaub4, t, rhi[0], rhi[1], rhi[2], rhi[3]);
+    }
+    s_lo[side] = inv_tap(kDaub4, t, p, ll[0], lh[0], ll[1], lh[1]);
+    s_hi[side] = inv_tap(kDaub4, t, p, hl[0], hh[0], hl[1], hh[1]);
+  }
+  const double v = inv_tap(kDaub4, t, q, s_lo[0], s_hi[0], s_lo[1], s_hi[1]);
+  return quantize_ref(__double2float_rn(v));
+}
+
+__device__ __forceinline__ double byte_at(const uint32_t (&w)[4], int k) {  // byte k of w[0..3]
+  return (double)((w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+}
+__device__ __forceinline__ double byte_at2(const uint32_t (&w)[2], int k) {
+  return (double)((w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+}
+
+// Recompute the queued unit (row pair i, first column c: output rows 2i,
+// 2i+1 x columns c .. c+7) in float64 and store its 16 bytes. fix_mode 2
+// (test hook): every pixel takes the reference-order path.
+__device__ __noinline__ void fix_unit_u8(const U8Band u, int i, int c) {
+  const int W = u.W, Wh = W >> 1, j = c >> 1;
+  const D4 tp = d4_taps();
+  const double h0 = tp.h0, h1 = tp.h1, h2 = tp.h2, h3 = tp.h3;
+  // MS rows i-1, i: bytes of half-columns j-4 .. j+3 (periodic in the window)
+  uint32_t mw[2][2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint8_t* row = u.ms_row(i - 1 + k);
+    if (j >= 4 && j + 4 <= Wh) {
+      mw[k][0] = __ldg(reinterpret_cast<const uint32_t*>(row + j - 4));
+      mw[k][1] = __ldg(reinterpret_cast<const uint32_t*>(row + j));
+    } else {
+      mw[k][0] = mw[k][1] = 0u;
+      for (int m = 0; m < 8; ++m)
+        mw[k][m >> 2] |= (uint32_t)__ldg(row + wrap(j - 4 + m, Wh)) << (8 * (m & 3));
+    }
+  }
+  // PAN rows 2i-2 .. 2i+3: bytes of columns c-4 .. c+11, one row at a time;
+  // rn[k][J] = row low-pass of row k at half-column j-1+J
+  double rn[6][5];
+  uint32_t pan_out[2][2];  // PAN bytes of the two output rows, columns c .. c+7
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const uint8_t* row = u.pan_row(2 * i - 2 + k);
+    uint32_t w[4];
+    if (c >= 4 && c + 12 <= W) {
+      w[0] = __ldg(reinterpret_cast<const uint32_t*>(row + c - 4));
+      const uint2 m = __ldg(reinterpret_cast<const uint2*>(row + c));
+      w[1] = m.x;
+      w[2] = m.y;
+      w[3] = __ldg(reinterpret_cast<const uint32_t*>(row + c + 8));
+    } else {
+      w[0] = w[1] = w[2] = w[3] = 0u;
+      for (int m = 0; m < 16; ++m)
+        w[m >> 2] |= (uint32_t)__ldg(row + wrap(c - 4 + m, W)) << (8 * (m & 3));
+    }
+    if (k == 2 || k == 3) {
+      pan_out[k - 2][0] = w[1];
+      pan_out[k - 2][1] = w[2];
+    }
+#pragma unroll
+    for (int J = 0; J < 5; ++J)  // columns c-2+2J .. c+1+2J = bytes 2+2J .. 5+2J
+      rn[k][J] = fma(h3, byte_at(w, 2 * J + 5),
+                     fma(h2, byte_at(w, 2 * J + 4),
+                         fma(h1, byte_at(w, 2 * J + 3), h0 * byte_at(w, 2 * J + 2))));
+  }
+  double v[2][5];  // vertical synthesis at output rows 2i, 2i+1, half-columns j-1 .. j+3
+#pragma unroll
+  for (int J = 0; J < 5; ++J) {
+    const double llm = fma(h3, rn[3][J], fma(h2, rn[2][J], fma(h1, rn[1][J], h0 * rn[0][J])));
+    const double llc = fma(h3, rn[5][J], fma(h2, rn[4][J], fma(h1, rn[3][J], h0 * rn[2][J])));
+    const double em = fma(2.0, byte_at2(mw[0], J + 3), -llm);  // half-column j-1+J = byte J+3
+    const double ec = fma(2.0, byte_at2(mw[1], J + 3), -llc);
+    v[0][J] = fma(h0, ec, h2 * em);
+    v[1][J] = fma(h1, ec, h3 * em);
+  }
+#pragma unroll
+  for (int pr = 0; pr < 2; ++pr) {
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int k = m >> 1;
+      const double syn = (m & 1) ? fma(h1, v[pr][k + 1], h3 * v[pr][k])
+                                 : fma(h0, v[pr][k + 1], h2 * v[pr][k]);
+      const double o = (double)((pan_out[pr][m >> 2] >> (8 * (m & 3))) & 0xffu) + syn;
+      uint32_t q = quantize_ref(__double2float_rn(o - 1e-9));
+      if (u.fix_mode == 2 || q != quantize_ref(__double2float_rn(o + 1e-9)))
+        q = ref_pixel_u8(u, 2 * i + pr, c + m);
+      w[m >> 2] |= q << (8 * (m & 3));
+    }
+    *reinterpret_cast<uint2*>(u.out + (long long)(2 * i + pr) * u.out_pitch + c) =
+        make_uint2(w[0], w[1]);
+  }
+}
+
+// The queued unit e = i << 11 | tt << 4 | b (row pair i, consumer thread tt,
+// band b) of the CTA whose column band starts at `base`
+template <int NB>
+__device__ __forceinline__ void fix_entry_u8(const FuseArgs<uint8_t>& a, uint32_t e, int base) {
+  fix_unit_u8(u8_band<NB>(a, (int)(e & 15u)), (int)(e >> 11), base + 8 * (int)((e >> 4) & 0x7fu));
+}
+
+template <int NB, int NCW, int MINB, int CVT, bool EXACT>
 __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
     fuse_d4_u8x8_kernel(const FuseArgs<uint8_t> a, int S) {
   constexpr int HALO = 16;
@@ -449,6 +665,11 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   // conflict-free), not in 5*NB registers: registers then fit 4 CTAs per SM
   float4* ep4 = reinterpret_cast<float4*>(empty + S) + t;  // [NB][NCW*32]
   float* ep1 = reinterpret_cast<float*>(reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + t;
+  // EXACT: this warp's queue of units to recompute (after the carry arrays)
+  uint32_t* fixq = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(
+                       reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + NB * NCW * 32) +
+                   warp * kU8FixCap;
+  int fixn = 0;  // queued units (warp-uniform)
 
 #pragma unroll 2
   for (int n = 0; n < nloads; ++n) {
@@ -510,33 +731,72 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
             V[J] = __ffma2_rn(H01, make_float2(e[J], e[J]),
                               __fmul2_rn(H23, make_float2(ep[J], ep[J])));
           float2 r[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int k = m >> 1;
-            const float2 o =
-                __fadd2_rn(pa[m], (m & 1) ? __ffma2_rn(H1, V[k + 1], __fmul2_rn(H3, V[k]))
-                                          : __ffma2_rn(H0, V[k + 1], __fmul2_rn(H2, V[k])));
-            // imageio.py:115-123 quantize as in quantize_lanes(), but with the
-            // magic 2^23 + 2^16: the low 16 bits of r are then floor(c) itself
-            // as a signed 16-bit lane (the 2^16 carries out), so the clamp
-            // needs no lane offset
-            r[m] = __fadd2_rd(__fadd2_rn(o, make_float2(0.5f, 0.5f)),
-                              make_float2(8454144.0f, 8454144.0f));
-          }
           uint32_t wq[2][2];
+          if constexpr (EXACT) {
+            // o + 0.5 + 2^-9 (the offset rides in pa) onto the 2^-8 grid,
+            // rounded down: bytes 1-2 = 0x4000 + integer part, byte 0 =
+            // fraction (see the v3 comment above fix_unit_u8)
 #pragma unroll
-          for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              const uint32_t l01 = __byte_perm(
-                  __float_as_uint(p ? r[4 * g].y : r[4 * g].x),
-                  __float_as_uint(p ? r[4 * g + 1].y : r[4 * g + 1].x), 0x5410);
-              const uint32_t l23 = __byte_perm(
-                  __float_as_uint(p ? r[4 * g + 2].y : r[4 * g + 2].x),
-                  __float_as_uint(p ? r[4 * g + 3].y : r[4 * g + 3].x), 0x5410);
-              wq[p][g] = __byte_perm(__vimin_s16x2_relu(l01, 0x00FF00FFu),
-                                     __vimin_s16x2_relu(l23, 0x00FF00FFu), 0x6420);
+            for (int m = 0; m < 8; ++m) {
+              const int k = m >> 1;
+              const float2 o = (m & 1) ? __ffma2_rn(H1, V[k + 1], __ffma2_rn(H3, V[k], pa[m]))
+                                       : __ffma2_rn(H0, V[k + 1], __ffma2_rn(H2, V[k], pa[m]));
+              r[m] = __fadd2_rd(o, make_float2(49152.0f, 49152.0f));
             }
+            uint32_t near = 0xFFFFFFFFu;  // min over (fraction byte : low integer byte) lanes
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+              for (int g = 0; g < 2; ++g) {
+                const uint32_t u0 = __float_as_uint(p ? r[4 * g].y : r[4 * g].x);
+                const uint32_t u1 = __float_as_uint(p ? r[4 * g + 1].y : r[4 * g + 1].x);
+                const uint32_t u2 = __float_as_uint(p ? r[4 * g + 2].y : r[4 * g + 2].x);
+                const uint32_t u3 = __float_as_uint(p ? r[4 * g + 3].y : r[4 * g + 3].x);
+                wq[p][g] = __byte_perm(
+                    __viaddmin_s16x2_relu(__byte_perm(u0, u1, 0x6521), 0xC000C000u, 0x00FF00FFu),
+                    __viaddmin_s16x2_relu(__byte_perm(u2, u3, 0x6521), 0xC000C000u, 0x00FF00FFu),
+                    0x6420);
+                near = __vimin3_u16x2(near, __byte_perm(u0, u1, 0x4501),
+                                      __byte_perm(u2, u3, 0x4501));
+              }
+            const bool flag = valid && a.fix_mode != 4 &&
+                              (a.fix_mode == 1 || a.fix_mode == 2 || (near & 0xFF00u) == 0u ||
+                               (near & 0xFF000000u) == 0u);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, flag);
+            if (bal) {  // warp-uniform
+              const int pos = fixn + __popc(bal & ((1u << lane) - 1u));
+              if (flag && pos < kU8FixCap)
+                fixq[pos] = ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b;
+              fixn += __popc(bal);
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+              const int k = m >> 1;
+              const float2 o =
+                  __fadd2_rn(pa[m], (m & 1) ? __ffma2_rn(H1, V[k + 1], __fmul2_rn(H3, V[k]))
+                                            : __ffma2_rn(H0, V[k + 1], __fmul2_rn(H2, V[k])));
+              // imageio.py:115-123 quantize as in quantize_lanes(), but with the
+              // magic 2^23 + 2^16: the low 16 bits of r are then floor(c) itself
+              // as a signed 16-bit lane (the 2^16 carries out), so the clamp
+              // needs no lane offset
+              r[m] = __fadd2_rd(__fadd2_rn(o, make_float2(0.5f, 0.5f)),
+                                make_float2(8454144.0f, 8454144.0f));
+            }
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+              for (int g = 0; g < 2; ++g) {
+                const uint32_t l01 = __byte_perm(
+                    __float_as_uint(p ? r[4 * g].y : r[4 * g].x),
+                    __float_as_uint(p ? r[4 * g + 1].y : r[4 * g + 1].x), 0x5410);
+                const uint32_t l23 = __byte_perm(
+                    __float_as_uint(p ? r[4 * g + 2].y : r[4 * g + 2].x),
+                    __float_as_uint(p ? r[4 * g + 3].y : r[4 * g + 3].x), 0x5410);
+                wq[p][g] = __byte_perm(__vimin_s16x2_relu(l01, 0x00FF00FFu),
+                                       __vimin_s16x2_relu(l23, 0x00FF00FFu), 0x6420);
+              }
+          }
           uint8_t* orow = a.out[0];
 #pragma unroll
           for (int bb = 1; bb < NB; ++bb)
@@ -549,15 +809,35 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
       }
     }
 #pragma unroll
-    for (int m = 0; m < 8; ++m) pa[m] = x[m + 2];
+    for (int m = 0; m < 8; ++m)
+      pa[m] = EXACT ? __fadd2_rn(x[m + 2], make_float2(0.5f + 0x1p-9f, 0.5f + 0x1p-9f))
+                    : x[m + 2];
 #pragma unroll
     for (int J = 0; J < 5; ++J) rprev[J] = rn[J];
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&empty[s]);
   }
+  if constexpr (EXACT) {
+    // The warp's queued units, recomputed in float64 once its row run is
+    // done (the loop above holds no state across this, so the fix-up's
+    // registers cost the streaming loop nothing; the task's rows are still
+    // in L2). The bytes were stored by this warp's lanes in the loop;
+    // __syncwarp orders those stores and the queue writes before the rewrites.
+    __syncwarp();
+    if (a.fix_mode == 3) return;  // timing experiment: detection only
+    if (fixn <= kU8FixCap) {
+      for (int k = lane; k < fixn; k += 32) fix_entry_u8<NB>(a, fixq[k], base);
+    } else if (valid) {
+      // queue overflow (inputs with many values at rounding boundaries):
+      // every unit of this lane's column group, all row pairs and bands
+      for (int i = i0; i < i1; ++i)
+        for (int b = 0; b < NB; ++b)
+          fix_entry_u8<NB>(a, ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b, base);
+    }
+  }
 }
 
-template <int NB, int NCW, int MINB, int CVT>
+template <int NB, int NCW, int MINB, int CVT, bool EXACT>
 static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
                                   const LaunchTuning& tune) {
   FuseArgs<uint8_t> a = a0;
@@ -567,10 +847,13 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   int S = tune.d4_stages > 0 ? tune.d4_stages : (int)((32 * 1024) / SLOT);
   if (S < 2) S = 2;
   if (S > 16) S = 16;
-  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer thread)
+  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer
+  // thread) + (EXACT) the per-warp fix-up queues
   const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
-                      (size_t)NB * NCW * 32 * 20;
-  auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT>;
+                      (size_t)NB * NCW * 32 * 20 +
+                      (EXACT ? (size_t)NCW * kU8FixCap * sizeof(uint32_t) : 0);
+  a.fix_mode = EXACT ? tune.u8_fix_mode : 0;
+  auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT, EXACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -585,23 +868,33 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   return cudaGetLastError();
 }
 
-static cudaError_t launch_u8x8(const FuseArgs<uint8_t>& a, cudaStream_t s,
-                               const LaunchTuning& tune) {
+template <bool EXACT>
+static cudaError_t launch_u8x8_v(const FuseArgs<uint8_t>& a, cudaStream_t s,
+                                 const LaunchTuning& tune) {
   // MS bytes converted on the ALU pipe, PAN bytes on the XU pipe: measured
   // best of the four splits (0.461 vs 0.473 ms for all-XU on a Landsat scene;
   // 3 CTAs/SM at 128 registers measured 0.509, 5 CTAs/SM at 72 registers
   // spill and measured 0.510)
   switch (a.nbands) {
-    case 1: return launch_u8x8_nb<1, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 2: return launch_u8x8_nb<2, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 3: return launch_u8x8_nb<3, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 4: return launch_u8x8_nb<4, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 5: return launch_u8x8_nb<5, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 6: return launch_u8x8_nb<6, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 7: return launch_u8x8_nb<7, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
-    case 8: return launch_u8x8_nb<8, 4, WF_U8X8_MIN_CTAS, 2>(a, s, tune);
+    case 1: return launch_u8x8_nb<1, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 2: return launch_u8x8_nb<2, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 3: return launch_u8x8_nb<3, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 4: return launch_u8x8_nb<4, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 5: return launch_u8x8_nb<5, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 6: return launch_u8x8_nb<6, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 7: return launch_u8x8_nb<7, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 8: return launch_u8x8_nb<8, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// 8 bpp D4: v3 (default) byte-exact with the float64 fix-up; WF_D4_U8=v2 the
+// round-1 kernel (bytes = quantize() of the float32 kernel, <= 1 LSB from the
+// reference); WF_D4_U8=v1 the 4-column kernel (same bytes as v2)
+static cudaError_t launch_u8x8(const FuseArgs<uint8_t>& a, cudaStream_t s,
+                               const LaunchTuning& tune) {
+  if (tune.d4_u8_variant == 2) return launch_u8x8_v<false>(a, s, tune);
+  return launch_u8x8_v<true>(a, s, tune);
 }
 
 template <typename T, int NB, int NCW>
@@ -644,7 +937,7 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
 template <typename T>
 cudaError_t launch_fuse_d4_tma(const FuseArgs<T>& a, cudaStream_t s, const LaunchTuning& tune) {
   if constexpr (sizeof(T) == 1) {
-    if (!tune.d4_u8_v1) return launch_u8x8(a, s, tune);  // WF_D4_U8=v1: the 4-column kernel
+    if (tune.d4_u8_variant != 1) return launch_u8x8(a, s, tune);  // WF_D4_U8=v1: 4 columns
   }
   switch (a.nbands) {
     case 1: return launch_tma_nb<T, 1, 4>(a, s, tune);

@@ -28,6 +28,7 @@ struct FuseArgs {
   long long out_pitch;
   int nbands;
   int wide;  // float64 with 32-byte aligned rows: 256-bit PAN loads / output stores
+  int fix_mode;  // 8 bpp D4 v3: 0 normal, 1 every unit re-done in float64, 2 in reference order
   int rows;  // PAN rows in this launch (even)
   int W;     // PAN columns (even)
   // filled by the launcher
@@ -43,7 +44,8 @@ struct LaunchTuning {
   int d4_stages;        // >0: shared-memory ring depth of the TMA kernel
   int haar_ppt;         // >0: Haar row pairs per thread (1, 2, 4, 8)
   int haar_u8_ppt;      // >0: 8 bpp Haar row pairs per thread
-  int d4_u8_v1;         // 1: the 4-column 8 bpp D4 kernel instead of the 8-column one
+  int d4_u8_variant;    // 8 bpp D4: 0 = v3 byte-exact (default), 1 = v1 (4 columns), 2 = v2
+  int u8_fix_mode;      // v3 test hook: 1 = recompute every unit, 2 = ... in reference order
   int d4_ldg;           // 1: force the register-path D4 kernel (no bulk copies)
   int no_wide;          // 1: float64 rows through 128-bit accesses, not 256-bit
   int exact_rows;       // >0: coefficient rows per CTA of the one-pass exact D4 kernel

@@ -351,14 +351,15 @@ def fuse_tile_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | No
 
 def fuse_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = None):
     """[quantize(p) for p in fuse_tile_quantized(pan_u8, ms_u8, method)]
-    (tiling.py:268-269) in ONE pass: uint8 PAN/MS in, uint8 out, float32
-    arithmetic with the quantize fused into the store (2.25 + 1.25 B per PAN
-    px per band instead of 9). Haar is bit-identical to the reference; D4 can
-    differ by one LSB where a value lies within ~1e-4 of a .5 boundary.
-    Shapes the 8 bpp kernels do not cover (MS not half size, W % 16 / 32)
-    take the float32 kernels plus the GPU quantize. exact=True (D4): the
-    reference-exact float64 sequence, then the quantize -- the reference
-    worker's bytes exactly (Haar's one-pass kernel already is)."""
+    (tiling.py:268-269) in ONE pass: uint8 PAN/MS in, uint8 out, the quantize
+    fused into the store (1 + 1.25 B per PAN px per band instead of 9), and
+    byte-identical to the reference worker in every mode: Haar is exact in
+    integer lanes; D4 computes in float32 with a proven error bound and
+    recomputes in float64 the 0.4% of pixels that lie near a rounding
+    boundary (csrc/fuse_tma.cu, v3). Shapes the 8 bpp kernels do not cover (MS
+    not half size, W % 16 / 32) take the reference-exact float64 kernels plus
+    the GPU quantize, which are byte-identical too. exact=True (D4) takes that
+    reference-order route for every pixel."""
     exact = _exact(exact)
     if not isinstance(method, DwtReplace):
         raise TypeError(f"unknown fusion method {method!r}")
@@ -395,8 +396,10 @@ def fuse_quantized(pan_u8, ms_u8, method: FusionMethod, *, exact: bool | None = 
                 ctx, code, pan_c.ctypes.data, _native.ptr_array([b.ctypes.data for b in band_c]),
                 _native.ptr_array([o.ctypes.data for o in outs]), len(bands), h, w))
         return outs
+    # bytes out: the reference-exact kernels, so the quantised bytes are the
+    # reference's whatever `exact` says
     fused = fuse_tile_quantized(_u8_device(pan_u8), [_u8_device(b) for b in bands], method,
-                                exact=exact)
+                                exact=True)
     outs = [_quantize_dev(f) for f in fused]
     return outs if is_t else [_device.to_host(o) for o in outs]
 

@@ -188,8 +188,11 @@ def fuse_pnm(pan: bytes, ms: list[bytes], method: FusionMethod, grid: tuple[int,
     GPU pipeline: raw payloads H2D -> planes with the edge padding of
     pad_inputs fused in (tiling.py:296-310) -> fuse_tiled on `grid` (per-tile
     wrap, tiling.py:213-273) -> crop + quantize + interleave -> D2H.
-    exact=True fuses every tile in the reference's float64 operation order,
-    which makes the output bytes identical to the reference CLI's."""
+    Every tile is fused in the reference's float64 operation order by
+    default (exact=None -> True here: the outputs are bytes, and they are the
+    reference CLI's bytes); exact=False takes the float32 kernels (within
+    1e-3 before the quantize, so a byte can differ by one where a value sits
+    at a rounding boundary)."""
     pr = PnmRaster.parse(pan)
     if pr.channels != 1:
         raise ValueError("panchromatic image must be grayscale")
@@ -215,7 +218,8 @@ def fuse_pnm(pan: bytes, ms: list[bytes], method: FusionMethod, grid: tuple[int,
         bh = (r.height * ph + h - 1) // h
         bw = (r.width * pw + w - 1) // w
         bands += [_plane_dev(t, c, bh, bw) for c in range(r.channels)]
-    fused = fuse_tiled(pan_t, bands, method, plan_grid(pw, ph, gw, gh), exact=exact)
+    fused = fuse_tiled(pan_t, bands, method, plan_grid(pw, ph, gw, gh),
+                       exact=True if exact is None else exact)
     if len(fused) == 3:
         return [write_pnm(_raster_from_planes(fused, h, w))]
     return [write_pnm(_raster_from_planes([f], h, w)) for f in fused]

@@ -250,8 +250,10 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
     output, pan dtype); exact=True fuses each tile in the reference's own
     float64 operation order (bit-identical to the reference). transfer_8bpp
     reproduces the distributed pipeline: inputs quantised to uint8
-    (wire_planes, tiling.py:192-210), each tile fused in float32 and quantised
-    (tiling.py:163-172, 268-269)."""
+    (wire_planes, tiling.py:192-210), each tile fused and quantised
+    (tiling.py:163-172, 268-269) -- byte-identical to the reference's workers
+    (the byte-exact 8 bpp kernels, or the reference-exact float64 kernels
+    plus the quantize for tile shapes they do not cover)."""
     exact = _exact(exact)
     if workers < 1:
         raise ValueError(f"workers {workers} must be >= 1")
@@ -291,11 +293,11 @@ def fuse_tiled(pan, ms, method: FusionMethod, grid: TileGrid, workers: int = 1,
         if _u8_windows_ok(grid, kind) and not (exact and kind is WaveletKind.DAUB4):
             outs = [torch.empty_like(pan_u8) for _ in ms_u8]
             _window_fuse(kind, pan_u8, ms_u8, outs, grid)
-        else:  # the float32 (or, exact, the reference's float64) kernels + quantize
+        else:  # the reference's float64 kernels + quantize: the worker's bytes
             pan_f = _u8_to_f32_dev(pan_u8)
             ms_f = [_u8_to_f32_dev(b) for b in ms_u8]
             fo = [torch.empty_like(pan_f) for _ in ms_f]
-            _window_fuse(kind, pan_f, ms_f, fo, grid, exact=exact)
+            _window_fuse(kind, pan_f, ms_f, fo, grid, exact=True)
             outs = [_quantize_dev(f) for f in fo]
         return outs if is_t else [_device.to_host(o) for o in outs]
 

@@ -108,7 +108,8 @@ def test_reference_suite_against_drop_in(ref):
     (ROOT / "gpurun_out" / "conformance_reference_suite.log").write_text(out + proc.stderr)
     passed = int(m.group(1)) if (m := re.search(r"(\d+) passed", out)) else 0
     failed = set(re.findall(r"FAILED \S*/tests/(\S+?)(?: - |\s|$)", out))
-    assert passed >= 175, out[-3000:]
     assert failed <= MATPLOTLIB_TESTS | TIMING_TESTS, failed
+    assert passed + len(failed) >= 178 and passed >= 178 - len(MATPLOTLIB_TESTS | TIMING_TESTS), \
+        out[-3000:]
     routed = re.search(r"B200 drop-in calls routed: (.*)", out)
     assert routed and "fuse_dwt=" in routed.group(1) and "worker_tiles=" in routed.group(1)

@@ -37,13 +37,22 @@ def test_fuse_pnm_exact_is_byte_identical(golden_pnm, name, method):
 
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("method", list(METHODS))
-def test_fuse_pnm_fused_kernels(golden_pnm, name, method):
-    """Default (fused float32 kernels): same headers and sizes; samples within
-    1 LSB of the reference (a float32 value can round across a .5 boundary),
-    and Haar on unresampled 8-bit input is exact (every value is a multiple
-    of 1/4)."""
+def test_fuse_pnm_default_byte_identical(golden_pnm, name, method):
+    """The default (no `exact` argument) writes the reference CLI's bytes."""
     pan, ms, grid = _inputs(golden_pnm, name)
     got = pnm.fuse_pnm(pan, ms, wf.DwtReplace(METHODS[method]), grid)
+    assert got == _outputs(golden_pnm, name, method)
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("method", list(METHODS))
+def test_fuse_pnm_fused_kernels(golden_pnm, name, method):
+    """exact=False (the fused float32 kernels): same headers and sizes;
+    samples within 1 LSB of the reference (a float32 value can round across
+    a .5 boundary), and Haar on unresampled 8-bit input is exact (every value
+    is a multiple of 1/4)."""
+    pan, ms, grid = _inputs(golden_pnm, name)
+    got = pnm.fuse_pnm(pan, ms, wf.DwtReplace(METHODS[method]), grid, exact=False)
     want = _outputs(golden_pnm, name, method)
     assert len(got) == len(want)
     for g, w in zip(got, want):

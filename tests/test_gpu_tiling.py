@@ -63,7 +63,7 @@ def test_d4_differences_confined_to_tile_border_band():
 @pytest.mark.parametrize("kname", list(KINDS))
 def test_transfer_8bpp_matches_reference(kname):
     """fuse_tiled(..., transfer_8bpp=True) (tiling.py:238-248) vs the
-    reference's own output: Haar bit-exact, D4 within one LSB."""
+    reference's own output: byte-exact, Haar and D4."""
     pan = Q8["tiled/pan"]
     ms = [Q8[f"tiled/ms{b}"] for b in range(3)]
     grid = wf.plan_grid(64, 64, 2, 2)
@@ -71,8 +71,7 @@ def test_transfer_8bpp_matches_reference(kname):
     for b, o in enumerate(got):
         ref = Q8[f"tiled/{kname}/out{b}"]
         assert o.dtype == np.uint8
-        d = np.abs(o.astype(np.int32) - ref.astype(np.int32))
-        assert d.max() <= (0 if kname == "haar" else 1)
+        assert np.array_equal(o, ref)
 
 
 def test_8bpp_tiles_aligned_for_the_u8_kernels():

@@ -20,7 +20,7 @@ mp = _native.ptr_array([m.data_ptr() for m in ms])
 op = _native.ptr_array([o.data_ptr() for o in out])
 nbytes = H * W + B * (H * W // 4 + H * W)
 # argv: configs "variant:pairs:stages" (0 = launcher default); D4 only when given
-configs = sys.argv[1:] or ["haar", "v2:32:0", "v2:16:0", "v2:64:0", "v1:32:0"]
+configs = sys.argv[1:] or ["haar", "v3:0:0", "v2:0:0", "v3:8:0", "v3:32:0"]
 for cfg in configs:
     if cfg == "haar":
         kind, variant, p, st = 1, "v2", 0, 0
@@ -30,6 +30,7 @@ for cfg in configs:
     os.environ["WF_D4_U8"] = variant
     os.environ["WF_D4_PAIRS"] = str(p)
     os.environ["WF_D4_STAGES"] = str(st)
+    _native.reload_tuning()
     if True:
         run = lambda: _native.check(lib.wf_fuse_bands_u8(kind, pan.data_ptr(), W, mp, W // 2, op,
                                                          W, B, H, W, None))
