@@ -51,7 +51,7 @@ static LaunchTuning read_tuning() {
   v.exact_rows = num("WF_EXACT_ROWS");
   v.exact_transforms = getenv("WF_EXACT_TRANSFORMS") != nullptr;
   const char* q = getenv("WF_QNR_KERNEL");
-  v.qnr_v1 = q && q[0] == 'v' && q[1] == '1';
+  v.qnr_kernel = (q && q[0] == 'v' && q[1] == '1') ? 1 : (q && q[0] == 'v' && q[1] == '3') ? 3 : 2;
   return v;
 }
 static LaunchTuning g_tuning = read_tuning();

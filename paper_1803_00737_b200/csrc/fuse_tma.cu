@@ -133,10 +133,19 @@ __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4], bool wide = 
 // (left halo + span) into ring slot n % S, with the transaction bytes on the
 // slot's full barrier. Slot layout: [PAN row | PAN row | NB x MS row], rows of
 // CW + 2*HALO and CW/2 + HALO elements.
-template <typename T, int NB, int CW, int HALO>
+template <typename T, int NB, int CW, int HALO, bool KEEP = false>
 __device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slots, uint64_t* full,
                                              uint64_t* empty, int base, int len, int i0,
                                              int nloads, int lane) {
+  // KEEP: the copies mark their lines evict_last in L2 (the 8 bpp fix-up
+  // re-reads the task's rows after the stream has moved on)
+  const uint64_t pol = KEEP ? tma::policy_evict_last() : 0ull;
+  auto g2s = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    if constexpr (KEEP)
+      tma::bulk_g2s_hint(dst, src, bytes, bar, pol);
+    else
+      tma::bulk_g2s(dst, src, bytes, bar);
+  };
   constexpr int PROW = CW + 2 * HALO;
   constexpr int MROW = CW / 2 + HALO;
   constexpr int SLOT = 2 * PROW + NB * MROW;
@@ -164,11 +173,11 @@ __device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slo
       const T* row = pan.row(2 * (i0 + k) + 2 + q);
       T* dst = slot + q * PROW;
       if (piece == 0)
-        tma::bulk_g2s(dst, row + lcol, HALO * sizeof(T), &full[s]);
+        g2s(dst, row + lcol, HALO * sizeof(T), &full[s]);
       else if (piece == 1)
-        tma::bulk_g2s(dst + HALO, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
+        g2s(dst + HALO, row + base, (uint32_t)(len * sizeof(T)), &full[s]);
       else
-        tma::bulk_g2s(dst + HALO + len, row + rcol, HALO * sizeof(T), &full[s]);
+        g2s(dst + HALO + len, row + rcol, HALO * sizeof(T), &full[s]);
     } else if (with_ms && lane < 6 + 2 * NB) {
       const int mrow = i0 + k;
       const T* mr = a.ms[0];
@@ -185,9 +194,9 @@ __device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slo
       }
       T* dst = slot + 2 * PROW + mb * MROW;
       if (mpiece == 0)
-        tma::bulk_g2s(dst, mr + mlcol, HALO * sizeof(T), &full[s]);
+        g2s(dst, mr + mlcol, HALO * sizeof(T), &full[s]);
       else
-        tma::bulk_g2s(dst + HALO, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)),
+        g2s(dst + HALO, mr + (base >> 1), (uint32_t)((len >> 1) * sizeof(T)),
                       &full[s]);
     }
   }
@@ -527,8 +536,12 @@ __device__ __forceinline__ double byte_at2(const uint32_t (&w)[2], int k) {
 
 // Recompute the queued unit (row pair i, first column c: output rows 2i,
 // 2i+1 x columns c .. c+7) in float64 and store its 16 bytes. fix_mode 2
-// (test hook): every pixel takes the reference-order path.
-__device__ __noinline__ void fix_unit_u8(const U8Band u, int i, int c) {
+// (test hook): every pixel takes the reference-order path. Inlined into the
+// kernel's tail (after the streaming loop, whose registers are dead there):
+// as a called function its frame and spills went to local memory, and with
+// the shared-memory carve-out leaving ~30 KB of L1 those round-trips ran at
+// L2 latency.
+__device__ __forceinline__ void fix_unit_u8(const U8Band& u, int i, int c) {
   const int W = u.W, Wh = W >> 1, j = c >> 1;
   const D4 tp = d4_taps();
   const double h0 = tp.h0, h1 = tp.h1, h2 = tp.h2, h3 = tp.h3;
@@ -546,61 +559,65 @@ __device__ __noinline__ void fix_unit_u8(const U8Band u, int i, int c) {
         mw[k][m >> 2] |= (uint32_t)__ldg(row + wrap(j - 4 + m, Wh)) << (8 * (m & 3));
     }
   }
-  // PAN rows 2i-2 .. 2i+3: bytes of columns c-4 .. c+11, one row at a time;
-  // rn[k][J] = row low-pass of row k at half-column j-1+J
-  double rn[6][5];
-  uint32_t pan_out[2][2];  // PAN bytes of the two output rows, columns c .. c+7
+  // PAN rows 2i-2 .. 2i+3: bytes of columns c-4 .. c+11
+  uint32_t w[6][4];
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     const uint8_t* row = u.pan_row(2 * i - 2 + k);
-    uint32_t w[4];
     if (c >= 4 && c + 12 <= W) {
-      w[0] = __ldg(reinterpret_cast<const uint32_t*>(row + c - 4));
+      w[k][0] = __ldg(reinterpret_cast<const uint32_t*>(row + c - 4));
       const uint2 m = __ldg(reinterpret_cast<const uint2*>(row + c));
-      w[1] = m.x;
-      w[2] = m.y;
-      w[3] = __ldg(reinterpret_cast<const uint32_t*>(row + c + 8));
+      w[k][1] = m.x;
+      w[k][2] = m.y;
+      w[k][3] = __ldg(reinterpret_cast<const uint32_t*>(row + c + 8));
     } else {
-      w[0] = w[1] = w[2] = w[3] = 0u;
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0u;
       for (int m = 0; m < 16; ++m)
-        w[m >> 2] |= (uint32_t)__ldg(row + wrap(c - 4 + m, W)) << (8 * (m & 3));
+        w[k][m >> 2] |= (uint32_t)__ldg(row + wrap(c - 4 + m, W)) << (8 * (m & 3));
     }
-    if (k == 2 || k == 3) {
-      pan_out[k - 2][0] = w[1];
-      pan_out[k - 2][1] = w[2];
-    }
-#pragma unroll
-    for (int J = 0; J < 5; ++J)  // columns c-2+2J .. c+1+2J = bytes 2+2J .. 5+2J
-      rn[k][J] = fma(h3, byte_at(w, 2 * J + 5),
-                     fma(h2, byte_at(w, 2 * J + 4),
-                         fma(h1, byte_at(w, 2 * J + 3), h0 * byte_at(w, 2 * J + 2))));
   }
   double v[2][5];  // vertical synthesis at output rows 2i, 2i+1, half-columns j-1 .. j+3
 #pragma unroll
   for (int J = 0; J < 5; ++J) {
-    const double llm = fma(h3, rn[3][J], fma(h2, rn[2][J], fma(h1, rn[1][J], h0 * rn[0][J])));
-    const double llc = fma(h3, rn[5][J], fma(h2, rn[4][J], fma(h1, rn[3][J], h0 * rn[2][J])));
+    double rn[6];  // row low-pass of rows 2i-2 .. 2i+3 at half-column j-1+J
+#pragma unroll
+    for (int k = 0; k < 6; ++k)  // columns c-2+2J .. c+1+2J = bytes 2+2J .. 5+2J
+      rn[k] = fma(h3, byte_at(w[k], 2 * J + 5),
+                  fma(h2, byte_at(w[k], 2 * J + 4),
+                      fma(h1, byte_at(w[k], 2 * J + 3), h0 * byte_at(w[k], 2 * J + 2))));
+    const double llm = fma(h3, rn[3], fma(h2, rn[2], fma(h1, rn[1], h0 * rn[0])));
+    const double llc = fma(h3, rn[5], fma(h2, rn[4], fma(h1, rn[3], h0 * rn[2])));
     const double em = fma(2.0, byte_at2(mw[0], J + 3), -llm);  // half-column j-1+J = byte J+3
     const double ec = fma(2.0, byte_at2(mw[1], J + 3), -llc);
     v[0][J] = fma(h0, ec, h2 * em);
     v[1][J] = fma(h1, ec, h3 * em);
   }
+  uint32_t esc = 0u;  // pixels too close to a byte boundary for any float64 order
 #pragma unroll
   for (int pr = 0; pr < 2; ++pr) {
-    uint32_t w[2] = {0u, 0u};
+    uint32_t q8[2] = {0u, 0u};
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int k = m >> 1;
       const double syn = (m & 1) ? fma(h1, v[pr][k + 1], h3 * v[pr][k])
                                  : fma(h0, v[pr][k + 1], h2 * v[pr][k]);
-      const double o = (double)((pan_out[pr][m >> 2] >> (8 * (m & 3))) & 0xffu) + syn;
-      uint32_t q = quantize_ref(__double2float_rn(o - 1e-9));
+      const double o = byte_at(w[2 + pr], m + 4) + syn;
+      const uint32_t q = quantize_ref(__double2float_rn(o - 1e-9));
       if (u.fix_mode == 2 || q != quantize_ref(__double2float_rn(o + 1e-9)))
-        q = ref_pixel_u8(u, 2 * i + pr, c + m);
-      w[m >> 2] |= q << (8 * (m & 3));
+        esc |= 1u << (8 * pr + m);
+      q8[m >> 2] |= q << (8 * (m & 3));
     }
     *reinterpret_cast<uint2*>(u.out + (long long)(2 * i + pr) * u.out_pitch + c) =
-        make_uint2(w[0], w[1]);
+        make_uint2(q8[0], q8[1]);
+  }
+  // the reference's own operation order for those (called only now, with
+  // nothing of the above live across the call)
+  while (esc) {
+    const int bit = __ffs(esc) - 1;
+    esc &= esc - 1u;
+    const int pr = bit >> 3, m = bit & 7;
+    u.out[(long long)(2 * i + pr) * u.out_pitch + c + m] =
+        (uint8_t)ref_pixel_u8(u, 2 * i + pr, c + m);
   }
 }
 
@@ -644,7 +661,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   __syncthreads();
 
   if (warp == NCW) {
-    produce_rows<uint8_t, NB, CW, HALO>(a, S, slots, full, empty, base, len, i0, nloads, lane);
+    produce_rows<uint8_t, NB, CW, HALO, EXACT>(a, S, slots, full, empty, base, len, i0, nloads,
+                                               lane);
     return;
   }
 
@@ -671,7 +689,10 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
                    warp * kU8FixCap;
   int fixn = 0;  // queued units (warp-uniform)
 
-#pragma unroll 2
+  // v2 unrolls the row-pair loop twice; v3's longer body is not unrolled (two
+  // copies overflowed the instruction cache: ncu's no_instruction stalls were
+  // a third of the samples)
+#pragma unroll(EXACT ? 1 : 2)
   for (int n = 0; n < nloads; ++n) {
     const int s = n % S;
     tma::mbar_wait_sleep(&full[s], (n / S) & 1);
@@ -825,14 +846,16 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
     // __syncwarp orders those stores and the queue writes before the rewrites.
     __syncwarp();
     if (a.fix_mode == 3) return;  // timing experiment: detection only
-    if (fixn <= kU8FixCap) {
-      for (int k = lane; k < fixn; k += 32) fix_entry_u8<NB>(a, fixq[k], base);
-    } else if (valid) {
-      // queue overflow (inputs with many values at rounding boundaries):
-      // every unit of this lane's column group, all row pairs and bands
-      for (int i = i0; i < i1; ++i)
-        for (int b = 0; b < NB; ++b)
-          fix_entry_u8<NB>(a, ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b, base);
+    // queued units, one per lane in turn; after a queue overflow (inputs with
+    // many values at rounding boundaries) every unit of this lane's column
+    // group instead, all row pairs and bands (one inlined copy of the fix-up)
+    const bool over = fixn > kU8FixCap;
+    const int cnt = over ? (valid ? (i1 - i0) * NB : 0) : (fixn - lane + 31) / 32;
+    for (int k = 0; k < cnt; ++k) {
+      const uint32_t e = over ? ((uint32_t)(i0 + k / NB) << 11) | ((uint32_t)t << 4) |
+                                    (uint32_t)(k % NB)
+                              : fixq[lane + 32 * k];
+      fix_entry_u8<NB>(a, e, base);
     }
   }
 }

@@ -1480,6 +1480,494 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
   if (FUSE && role == 0 && lane == 0) tma::bulk_wait<0>();  // fused-band stores complete
 }
 
+// ---------------------------------------------------------------------------
+// v3 (opt-in, WF_QNR_KERNEL=v3): one warp per PAIR of 32x32 blocks side by side (lanes
+// 0-15: the left block, 16-31: the right one), each lane owning two adjacent
+// columns -- one 2x2 cell column -- and the warp marching down a run of block
+// rows with its own cp.async ring. No warp roles, no producer warp, no
+// barriers between warps (the v2 kernel's ring handshakes between role warps
+// and per-tile barriers were most of its time). Per row pair a lane:
+//   * issues the cp.async (LDGSTS) copies of row pair n + S - 1: one 16-byte
+//     piece of each fused band's and the PAN's two 64-column rows, and MS row
+//     n + S over the 32 MS columns plus one (clamped) halo column each side;
+//   * forms U_k = bilinear(M_k) at its two columns in the reference's order
+//     -- horizontal along MS row n + 1, then vertical between carried rows
+//     (resample_bilinear, fusion.py:67-81; difference form, so constant
+//     regions stay exactly constant), two columns per FFMA2;
+//   * accumulates the 68 shifted first/second moments of {F_k, U_k, P} over
+//     its 4 pixels in float32 (shift = the block's first pixel);
+//   * does its own 2x2 cell for every band: the ERGAS sums in float64 (a 2x2
+//     sum of float32 values is exact there, metrics.py:37-42,117) and the
+//     shifted low-resolution D_s moments of (M_k, degrade(P)).
+// At the end of a block row each half-warp reduces its 100 per-lane values
+// (float32 transposed shuffle tree over 16 lanes, then float64), scores its
+// block's Q pairs (q_from_sums, the reference's den == 0 rule) and writes the
+// same per-block partials as v1/v2, so the edge and finish kernels are shared.
+//
+// Measured on the Landsat scene (tools/time_qnr_variants.py, ncu
+// profiles/r02_qnr_v3.md): 2.40 ms per report against v2's 2.02 ms, so v2 stays
+// the default. The kernel executes 1.42 G warp instructions (~810 per row pair
+// and warp: 4 pixels x ~70 for the moments, plus addressing, cells and the
+// block reductions) at IPC 2.1 with 8 warps per SM (255 registers, small
+// spills); a one-column-per-lane variant with 12 warps per SM ran 1.95 G
+// instructions at IPC 2.4 (2.82 ms). The report is the same to ~1e-10.
+// ---------------------------------------------------------------------------
+#ifndef WF_Q3_WARPS  // independent warps per CTA
+#define WF_Q3_WARPS 4
+#endif
+#ifndef WF_Q3_MINB  // CTAs per SM the registers are sized for (4 warps x 2 = 8 warps, <= 255 regs)
+#define WF_Q3_MINB 2
+#endif
+#ifndef WF_Q3_STAGES  // ring depth in row pairs (6 fits 2 CTAs of 4 warps per SM)
+#define WF_Q3_STAGES 6
+#endif
+#ifndef WF_Q3_RUN  // block rows per warp task
+#define WF_Q3_RUN 8
+#endif
+
+template <int NB>
+struct Q3Cfg {
+  static constexpr int S = WF_Q3_STAGES;
+  static constexpr int NPL = NB + 1;               // staged PAN-resolution planes: F.., P
+  static constexpr int PLANE = 128;                // [row][64 columns]
+  static constexpr int MOFF = NPL * PLANE;
+  static constexpr int MSEG = 40;                  // [3] = col m0-1, [4..35] = m0.., [36] = m0+32
+  static constexpr int STAGE = MOFF + NB * MSEG;   // floats per row-pair stage
+  static constexpr int NF = 2 * NB + 1 + 2 * (NB * (NB + 1) / 2) + 2 * NB + 1;  // 68 at NB = 6
+  static constexpr int NLOW = 3 * NB + 2;
+  static constexpr int NRED = NF + NLOW + 2 * NB;  // + low-res + ERGAS = 100
+  static constexpr int NRED_PAD = (NRED + 15) / 16 * 16;
+};
+
+template <int NB>
+static size_t q3_smem() {
+  using C = Q3Cfg<NB>;
+  return 16 + (size_t)WF_Q3_WARPS *
+                  ((size_t)C::S * C::STAGE * sizeof(float) + (size_t)2 * C::NRED * sizeof(double));
+}
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, neg2(b)); }
+
+template <int NB>
+__global__ void __launch_bounds__(32 * WF_Q3_WARPS, WF_Q3_MINB)
+    quality_tile_kernel(const QsArgs a, double* part_q, double* part_low, double* part_erg,
+                        int* undecidable) {
+  using L = QsLayout<NB>;
+  using C = Q3Cfg<NB>;
+  constexpr int S = C::S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4;
+  float* ring = reinterpret_cast<float*>(smem_raw) + (size_t)warp * S * C::STAGE;
+  double* red = reinterpret_cast<double*>(reinterpret_cast<float*>(smem_raw) +
+                                          (size_t)WF_Q3_WARPS * S * C::STAGE) +
+                (size_t)warp * 2 * C::NRED + half * C::NRED;
+  const int ncp = (a.nbc + 1) >> 1;  // block-column pairs
+  const int runs = (a.nbr + WF_Q3_RUN - 1) / WF_Q3_RUN;
+  const int task = blockIdx.x * WF_Q3_WARPS + warp;
+  if (task >= runs * ncp) return;
+  const int cp = task % ncp, run = task / ncp;
+  const int bi0 = run * WF_Q3_RUN, bi1 = min(bi0 + WF_Q3_RUN, a.nbr);
+  const int c0 = 64 * cp, m0 = 32 * cp;
+  const int n0 = 16 * bi0, npairs = 16 * (bi1 - bi0);
+  const int bj = 2 * cp + half;
+  const bool right_ok = 2 * cp + 1 < a.nbc;  // the right block exists
+  const bool mine_ok = half == 0 || right_ok;
+
+  // ---- copy roles, fixed for the task ----
+  // PAN-resolution planes: lane -> row lane >> 4, 16-byte piece lane & 15
+  // (pieces 8..15 are the right block's: skipped when it does not exist)
+  const bool piece_ok = (lane & 15) < 8 || right_ok;
+  const long long lane_off = (long long)(lane >> 4) * a.fp + c0 + 4 * (lane & 15);
+  float* const lane_dst = ring + (lane >> 4) * 64 + 4 * (lane & 15);
+  // MS segment: 16-byte pieces when the 32 columns lie inside the plane,
+  // else 4-byte copies of clamped columns (the scene's right edge)
+  const bool ms_vec = m0 + 32 <= a.Wh;
+  const int hl = max(m0 - 1, 0), hr = min(m0 + 32, a.Wh - 1);
+  const int mc4 = min(m0 + lane, a.Wh - 1);
+  int slot_w = 0;  // ring slot the next issue writes
+  auto issue = [&](int t) {  // row pair n0 + t
+    if (t < npairs) {
+      float* slot = ring + slot_w * C::STAGE;
+      const long long row = (long long)(2 * (n0 + t)) * a.fp + lane_off;
+      float* dst = lane_dst + slot_w * C::STAGE;
+      if (piece_ok) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) cp_async16(dst + k * C::PLANE, a.F[k] + row);
+        cp_async16(dst + NB * C::PLANE, a.P + row);
+      }
+      const long long mrow = (long long)min(n0 + t + 1, a.Hh - 1) * a.mp;
+      float* mdst = slot + C::MOFF;
+      if (ms_vec) {
+        if (lane < 8) {
+#pragma unroll
+          for (int k = 0; k < NB; ++k)
+            cp_async16(mdst + k * C::MSEG + 4 + 4 * lane, a.M[k] + mrow + m0 + 4 * lane);
+        } else if (lane < 10) {
+#pragma unroll
+          for (int k = 0; k < NB; ++k)
+            cp_async4(mdst + k * C::MSEG + (lane == 8 ? 3 : 36), a.M[k] + mrow + (lane == 8 ? hl : hr));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          cp_async4(mdst + k * C::MSEG + 4 + lane, a.M[k] + mrow + mc4);
+          if (lane < 2) cp_async4(mdst + k * C::MSEG + (lane == 0 ? 3 : 36), a.M[k] + mrow + (lane == 0 ? hl : hr));
+        }
+      }
+      slot_w = slot_w + 1 == S ? 0 : slot_w + 1;
+    }
+    cp_async_commit();  // empty groups keep the group count uniform
+  };
+  for (int t = 0; t < S - 1; ++t) issue(t);
+
+  // MS rows n0-1, n0 (clamped), horizontally interpolated at this lane's two
+  // columns; the raw MS row n0 at its cell column m
+  const int m = m0 + lane;
+  const int xa = min(max(m - 1, 0), a.Wh - 1), xb = min(m, a.Wh - 1), xc = min(m + 1, a.Wh - 1);
+  const float2 FX = f2(0.75f, 0.25f);
+  float2 hp[NB], hc[NB];
+  float mraw[NB];
+  auto hinterp = [&](float va, float vb, float vc) {  // (col 2m, col 2m+1)
+    return __ffma2_rn(FX, sub2(f2(vb, vc), f2(va, vb)), f2(va, vb));
+  };
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const float* r0 = a.M[k] + (long long)max(n0 - 1, 0) * a.mp;
+    const float* r1 = a.M[k] + (long long)n0 * a.mp;
+    hp[k] = hinterp(__ldg(r0 + xa), __ldg(r0 + xb), __ldg(r0 + xc));
+    const float v1 = __ldg(r1 + xb);
+    hc[k] = hinterp(__ldg(r1 + xa), v1, __ldg(r1 + xc));
+    mraw[k] = v1;
+  }
+
+  // ---- per-block state ----
+  float kF[NB], kU[NB], kP = 0.f, km[NB];
+  double kdp = 0.0;
+  float s1[2 * NB + 1];
+  float2 ffp[NB * (NB + 1) / 4 + NB], uup[NB * (NB + 1) / 4 + NB];  // packed triangles
+  float ffs[NB], uus[NB];                                          // unpaired entries
+  float2 fu2[(NB + 1) / 2], fp2[(NB + 1) / 2];
+  float pp;
+  float l1m[NB], lmm[NB], lmp[NB], l1p, lpp, summ[NB];
+  double sse[NB];
+  auto reset = [&]() {
+#pragma unroll
+    for (int i = 0; i < 2 * NB + 1; ++i) s1[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < NB * (NB + 1) / 4 + NB; ++i) ffp[i] = uup[i] = f2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      ffs[i] = uus[i] = 0.f;
+      l1m[i] = lmm[i] = lmp[i] = summ[i] = 0.f;
+      sse[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < (NB + 1) / 2; ++i) fu2[i] = fp2[i] = f2(0.f, 0.f);
+    pp = l1p = lpp = 0.f;
+  };
+  reset();
+
+  // the moments of one pixel: d = value - shift, products accumulated in band
+  // pairs (FFMA2 with the broadcast operand)
+  auto moments = [&](const float (&f)[NB], const float (&u)[NB], float p) {
+    float dF[NB + 1], dU[NB + 1];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      dF[k] = f[k] - kF[k];
+      dU[k] = u[k] - kU[k];
+      s1[k] += dF[k];
+      s1[NB + k] += dU[k];
+    }
+    dF[NB] = dU[NB] = 0.f;
+    const float dP = p - kP;
+    s1[2 * NB] += dP;
+    int pi = 0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      int l = k;
+      if (k & 1) {
+        ffs[k] = fmaf(dF[k], dF[k], ffs[k]);
+        uus[k] = fmaf(dU[k], dU[k], uus[k]);
+        ++l;
+      }
+      const float2 bf = f2(dF[k], dF[k]), bu = f2(dU[k], dU[k]);
+#pragma unroll
+      for (; l < NB; l += 2, ++pi) {
+        ffp[pi] = __ffma2_rn(bf, f2(dF[l], dF[l + 1]), ffp[pi]);
+        uup[pi] = __ffma2_rn(bu, f2(dU[l], dU[l + 1]), uup[pi]);
+      }
+    }
+    const float2 bp = f2(dP, dP);
+#pragma unroll
+    for (int k = 0; k < NB; k += 2) {
+      fu2[k / 2] = __ffma2_rn(f2(dF[k], dF[k + 1]), f2(dU[k], dU[k + 1]), fu2[k / 2]);
+      fp2[k / 2] = __ffma2_rn(f2(dF[k], dF[k + 1]), bp, fp2[k / 2]);
+    }
+    pp = fmaf(dP, dP, pp);
+  };
+
+  int slot_r = 0;
+  for (int t = 0; t < npairs; ++t) {
+    issue(t + S - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const float* st = ring + slot_r * C::STAGE;
+    slot_r = slot_r + 1 == S ? 0 : slot_r + 1;
+    const int tb = t & 15;  // row pair within the block
+    const int bi = bi0 + (t >> 4);
+    // this lane's two columns of every staged plane, both rows
+    float2 g0[NB], g1[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      g0[k] = *reinterpret_cast<const float2*>(st + k * C::PLANE + 2 * lane);
+      g1[k] = *reinterpret_cast<const float2*>(st + k * C::PLANE + 64 + 2 * lane);
+    }
+    const float2 q0 = *reinterpret_cast<const float2*>(st + NB * C::PLANE + 2 * lane);
+    const float2 q1 = *reinterpret_cast<const float2*>(st + NB * C::PLANE + 64 + 2 * lane);
+    // MS row n + 1: horizontal interpolation; vertical for rows 2n, 2n+1
+    float2 u0[NB], u1[NB];
+    float mnext[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const float* seg = st + C::MOFF + k * C::MSEG + 3 + lane;  // col m - 1
+      const float va = seg[0], vb = seg[1], vc = seg[2];
+      mnext[k] = vb;
+      const float2 hn = hinterp(va, vb, vc);
+      u0[k] = __ffma2_rn(f2(0.75f, 0.75f), sub2(hc[k], hp[k]), hp[k]);  // MS rows n-1, n
+      u1[k] = __ffma2_rn(f2(0.25f, 0.25f), sub2(hn, hc[k]), hc[k]);     // MS rows n, n+1
+      hp[k] = hc[k];
+      hc[k] = hn;
+    }
+    const bool low_ok = (bi >> 1) < a.nbr_l && (bj >> 1) < a.nbc_l;
+    if (tb == 0) {
+      // block start: the shifts -- the block's first pixel (lane 16 * half,
+      // row 2n, its first column) and the low-resolution block's first cell
+      const int src = lane & 16;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        kF[k] = __shfl_sync(0xffffffffu, g0[k].x, src);
+        kU[k] = __shfl_sync(0xffffffffu, u0[k].x, src);
+      }
+      kP = __shfl_sync(0xffffffffu, q0.x, src);
+      const int lr = bi >> 1, lc = min(bj >> 1, max(a.nbc_l - 1, 0));
+      const long long pr = (long long)(64 * lr) * a.pp + 64 * lc;
+      if (low_ok) {
+        kdp = (((double)__ldg(a.P + pr) + (double)__ldg(a.P + pr + 1)) +
+               ((double)__ldg(a.P + pr + a.pp) + (double)__ldg(a.P + pr + a.pp + 1))) * 0.25;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) km[k] = __ldg(a.M[k] + (long long)(32 * lr) * a.mp + 32 * lc);
+      }
+    }
+    {
+      float f[NB], u[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) { f[k] = g0[k].x; u[k] = u0[k].x; }
+      moments(f, u, q0.x);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) { f[k] = g0[k].y; u[k] = u0[k].y; }
+      moments(f, u, q0.y);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) { f[k] = g1[k].x; u[k] = u1[k].x; }
+      moments(f, u, q1.x);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) { f[k] = g1[k].y; u[k] = u1[k].y; }
+      moments(f, u, q1.y);
+    }
+    // this lane's 2x2 cell: ERGAS for every band, and the low-resolution
+    // D_s moments when the block lies in the low-resolution grid
+    const double dp = (((double)q0.x + (double)q0.y) + ((double)q1.x + (double)q1.y)) * 0.25;
+    const float ddp = low_ok ? (float)(dp - kdp) : 0.f;
+    l1p += ddp;
+    lpp = fmaf(ddp, ddp, lpp);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const double sk = ((double)g0[k].x + (double)g0[k].y) + ((double)g1[k].x + (double)g1[k].y);
+      const double e = fma(sk, 0.25, -(double)mraw[k]);
+      sse[k] = fma(e, e, sse[k]);
+      summ[k] += mraw[k];
+      const float dm = low_ok ? mraw[k] - km[k] : 0.f;
+      l1m[k] += dm;
+      lmm[k] = fmaf(dm, dm, lmm[k]);
+      lmp[k] = fmaf(dm, ddp, lmp[k]);
+      mraw[k] = mnext[k];
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+
+    if (tb == 15) {
+      // ---- block end: reduce (per half-warp), score, write the partials ----
+      float v[C::NRED_PAD];
+      int r = 0;
+#pragma unroll
+      for (int i = 0; i < 2 * NB + 1; ++i) v[r++] = s1[i];
+      {
+        int pi = 0;
+        float ff[NB][NB], uu[NB][NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          int l = k;
+          if (k & 1) {
+            ff[k][k] = ffs[k];
+            uu[k][k] = uus[k];
+            ++l;
+          }
+#pragma unroll
+          for (; l < NB; l += 2, ++pi) {
+            ff[k][l] = ffp[pi].x;
+            uu[k][l] = uup[pi].x;
+            if (l + 1 < NB) {
+              ff[k][l + 1] = ffp[pi].y;
+              uu[k][l + 1] = uup[pi].y;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) v[2 * NB + 1 + L::tri(k, l)] = ff[k][l];
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) v[2 * NB + 1 + L::NFF + L::tri(k, l)] = uu[k][l];
+        r = 2 * NB + 1 + 2 * L::NFF;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fu2[k / 2].y : fu2[k / 2].x;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fp2[k / 2].y : fp2[k / 2].x;
+        v[r++] = pp;
+      }
+      // low-res [S1m[NB] S1p S2mm[NB] S2pp S2mp[NB]], ERGAS [sse[NB] summ[NB]]
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[r++] = l1m[k];
+      v[r++] = l1p;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[r++] = lmm[k];
+      v[r++] = lpp;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[r++] = lmp[k];
+      constexpr int SSE0 = C::NF + C::NLOW;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[r++] = 0.f;  // the float64 squares go separately
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[r++] = summ[k];
+#pragma unroll
+      for (; r < C::NRED_PAD; ++r) v[r] = 0.f;
+      // half-warp sums: groups of 16 values transposed down a 4-level shuffle
+      // tree -- lane j of a half ends with value 16g + j summed over its 16
+      // lanes (float32: sums of <= 1024 shifted products), then float64
+#pragma unroll
+      for (int g = 0; g < C::NRED_PAD / 16; ++g) {
+        float x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = v[16 * g + i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const float send = up ? x[i] : x[i + o];
+            const float keep = up ? x[i + o] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        const int j = 16 * g + (lane & 15);
+        if (j < C::NRED && (j < SSE0 || j >= SSE0 + NB)) red[j] = (double)x[0];
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        double x = sse[k];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((lane & 15) == k) red[SSE0 + k] = x;
+      }
+      __syncwarp();
+      if (mine_ok) {
+        const size_t blk = (size_t)bi * a.nbc + bj, nparts = (size_t)a.nbr * a.nbc;
+        constexpr int CP = NB * (NB - 1) / 2;
+        const int base2 = 2 * NB + 1;
+        for (int q = lane & 15; q < L::NQ; q += 16) {
+          int pa_, pb_, saa, sbb, sab;
+          if (q < NB) {
+            pa_ = q;
+            pb_ = NB + q;
+            saa = L::tri(q, q);
+            sbb = L::NFF + L::tri(q, q);
+            sab = 2 * L::NFF + q;
+          } else if (q < NB + 2 * CP) {
+            int p = (q - NB) % CP, k = 0;
+            const int off = (q - NB) < CP ? 0 : 1;
+            while (p >= NB - 1 - k) {
+              p -= NB - 1 - k;
+              ++k;
+            }
+            const int l = k + 1 + p;
+            pa_ = off * NB + k;
+            pb_ = off * NB + l;
+            saa = off * L::NFF + L::tri(k, k);
+            sbb = off * L::NFF + L::tri(l, l);
+            sab = off * L::NFF + L::tri(k, l);
+          } else {
+            const int k = q - NB - 2 * CP;
+            pa_ = k;
+            pb_ = 2 * NB;
+            saa = L::tri(k, k);
+            sbb = 2 * L::NFF + 2 * NB;
+            sab = 2 * L::NFF + NB + k;
+          }
+          auto shift = [&](int plane) -> double {
+            float x = kP;
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+              if (plane == k) x = kF[k];
+              if (plane == NB + k) x = kU[k];
+            }
+            return (double)x;
+          };
+          part_q[(size_t)q * nparts + blk] =
+              q_from_sums(1024.0, shift(pa_), shift(pb_), red[pa_], red[pb_], red[base2 + saa],
+                          red[base2 + sbb], red[base2 + sab], undecidable);
+        }
+        if (low_ok) {
+          const size_t nlow = (size_t)a.nbr_l * a.nbc_l;
+          double* dst = part_low +
+                        (size_t)((bi & 1) * 2 + (bj & 1)) * (L::NLOW + NB + 1) * nlow +
+                        (size_t)((bi >> 1) * a.nbc_l + (bj >> 1));
+          for (int k = lane & 15; k < L::NLOW; k += 16) dst[k * nlow] = red[C::NF + k];
+          // the shifts (the finish kernel reads quadrant 0's slots; all four
+          // quadrants used the low-resolution block's first cell)
+          if ((lane & 15) < NB) {
+            float x = 0.f;
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+              if ((lane & 15) == k) x = km[k];
+            dst[(L::NLOW + (lane & 15)) * nlow] = (double)x;
+          }
+          if ((lane & 15) == 0) dst[(L::NLOW + NB) * nlow] = kdp;
+        }
+        for (int k = lane & 15; k < L::NERG; k += 16) part_erg[k * nparts + blk] = red[SSE0 + k];
+      }
+      __syncwarp();
+      reset();
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ---- host side ---------------------------------------------------------------
 constexpr int kEdgeCtas = 256;
 
@@ -1494,7 +1982,8 @@ static size_t qs_smem() {
 
 // Which scene kernel runs: the role-split one (default) or, with
 // WF_QNR_KERNEL=v1, the one-warp-per-block one (kept for A/B timing).
-static bool qs_use_v1() { return env_tuning().qnr_v1 != 0; }
+static bool qs_use_v1() { return env_tuning().qnr_kernel == 1; }
+static bool qs_use_v3() { return env_tuning().qnr_kernel == 3; }
 
 template <int NB, bool FUSE>
 static size_t q2_smem() {
@@ -1631,7 +2120,43 @@ static cudaError_t launch_qs_nb(const float* const* F, const float* const* M, co
   a.Hh = h / 2;
   a.Wh = w / 2;
   const bool v1 = !fuse && qs_use_v1();
+  // v3 (WF_QNR_KERNEL=v3): cp.async copies of 16-byte pieces of the fused and
+  // PAN rows, which share one pitch
+  bool v3 = !fuse && !v1 && qs_use_v3() && fp == pp && fp % 4 == 0 &&
+            (reinterpret_cast<uintptr_t>(P) & 15u) == 0;
+  for (int k = 0; v3 && k < NB; ++k) v3 = (reinterpret_cast<uintptr_t>(F[k]) & 15u) == 0;
   qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, a.ncx, v1 ? kQsWarps : kQ2Bc);
+  if (v3) {
+    const int nparts3 = a.nbr * a.nbc;  // per-block partials
+    double* pq = static_cast<double*>(workspace);
+    double* pl = pq + (size_t)nparts3 * L::NQ;
+    double* pe = pl + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
+    double* pg = pe + (size_t)nparts3 * L::NERG;
+    double* fin3 = pg + (size_t)kEdgeCtas * 2 * NB;
+    const size_t smem3 = q3_smem<NB>();
+    cudaError_t e3 = cudaFuncSetAttribute(quality_tile_kernel<NB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+    if (e3 != cudaSuccess) return e3;
+    if ((e3 = cudaMemsetAsync(undecidable, 0, sizeof(int), s)) != cudaSuccess) return e3;
+    const int runs = (a.nbr + WF_Q3_RUN - 1) / WF_Q3_RUN;
+    const int tasks = runs * ((a.nbc + 1) / 2);
+    const int ctas = (tasks + WF_Q3_WARPS - 1) / WF_Q3_WARPS;
+    if (ctas > 0)
+      quality_tile_kernel<NB><<<ctas, 32 * WF_Q3_WARPS, smem3, s>>>(a, pq, pl, pe, undecidable);
+    if ((e3 = cudaGetLastError()) != cudaSuccess) return e3;
+    const int row_lo = 16 * a.nbr, col_lo = 16 * a.nbc;
+    int nedge3 = 0;
+    if (row_lo < a.Hh || col_lo < a.Wh) {
+      nedge3 = kEdgeCtas;
+      quality_edge_kernel<NB><<<nedge3, 256, 0, s>>>(a, row_lo, col_lo, pg);
+      if ((e3 = cudaGetLastError()) != cudaSuccess) return e3;
+    }
+    quality_finish_kernel<NB><<<dim3(L::NQ + 3 * NB, kFinSplit), kFinThreads, 0, s>>>(
+        a, pq, nparts3, pl, pe, pg, nedge3, fin3, undecidable);
+    if ((e3 = cudaGetLastError()) != cudaSuccess) return e3;
+    quality_finish2_kernel<NB><<<1, 128, 0, s>>>(a, fin3, out);
+    return cudaGetLastError();
+  }
   const int ncta = a.nbr * a.ncx;  // tiles
   const int nparts = v1 ? ncta : ncta * kQ2Bc;  // Q / ERGAS partials
   double* part_q = static_cast<double*>(workspace);

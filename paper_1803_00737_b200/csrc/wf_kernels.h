@@ -50,7 +50,7 @@ struct LaunchTuning {
   int no_wide;          // 1: float64 rows through 128-bit accesses, not 256-bit
   int exact_rows;       // >0: coefficient rows per CTA of the one-pass exact D4 kernel
   int exact_transforms; // 1: exact mode as forward + inverse transform kernels
-  int qnr_v1;           // 1: the one-warp-per-block QNR scene kernel
+  int qnr_kernel;       // QNR scene kernel: 2 = v2 role-split (default), 1 = v1, 3 = v3 (tile)
 };
 
 // The tuning knobs of the environment (WF_HAAR_PPT, WF_D4_*, ...), read once
