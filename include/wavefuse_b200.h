@@ -299,6 +299,14 @@ int64_t wf_quality_scene_workspace_bytes(int nbands, int h, int w);
 int wf_quality_scene_f32(const float* const* fused, const float* const* ms, const float* pan,
                          int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
                          int w, void* workspace, double* out, int* undecidable, void* stream);
+/* The same report for a float64 scene (the planes a float64 numpy caller's
+ * fuse() returns, fusion.py:46-47): float64 shifts, upsampling and 2x2 cells,
+ * float32 shifted moments -- the precision of the float32 path. Same output
+ * layout and workspace; the fused bands and the PAN share one pitch; 16-byte
+ * aligned rows. */
+int wf_quality_scene_f64(const double* const* fused, const double* const* ms, const double* pan,
+                         int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
+                         int w, void* workspace, double* out, int* undecidable, void* stream);
 /* SURVEY.md 8(f) row f1, second half: Haar fusion and its quality report in
  * ONE pass over the scene -- fusion.py:153-183 fuse(pan, ms, DwtReplace(HAAR))
  * followed by metrics.py:178-199 qnr(fused, ms, pan), without re-reading the

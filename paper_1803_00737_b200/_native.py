@@ -117,6 +117,8 @@ def _declare_quality(lib: ctypes.CDLL) -> None:
         "wf_quality_scene_workspace_bytes": ([c_int, c_int, c_int], c_i64),
         "wf_quality_scene_f32": ([c_vpp, c_vpp, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_int,
                                   c_vp, c_vp, c_vp, c_vp], c_int),
+        "wf_quality_scene_f64": ([c_vpp, c_vpp, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_int,
+                                  c_vp, c_vp, c_vp, c_vp], c_int),
         "wf_ergas_band": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_int, c_int, c_int, c_vp,
                            c_vp, c_vp], c_int),
         "wf_fuse_quality_f32": ([c_int, c_vp, c_i64, c_vpp, c_i64, c_vpp, c_i64, c_int, c_int,

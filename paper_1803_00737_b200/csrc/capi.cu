@@ -1032,6 +1032,33 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
   return cuda_status(e, "wf_quality_scene_f32");
 }
 
+int wf_quality_scene_f64(const double* const* fused, const double* const* ms, const double* pan,
+                         int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
+                         int w, void* workspace, double* out, int* undecidable, void* stream) {
+  if (!fused || !ms || !pan || !workspace || !out || !undecidable)
+    return fail(WF_ERR_VALUE, "null pointer argument");
+  if (nbands < 2 || nbands > wf::kMaxBandsPerLaunch)
+    return fail(WF_ERR_BAND_COUNT, "fused quality path takes 2..%d bands, got %d",
+                wf::kMaxBandsPerLaunch, nbands);
+  if ((h & 1) || (w % 8) || h < 64 || w < 64)
+    return fail(WF_ERR_VALUE, "fused quality path needs even H, W % 8 == 0, H, W >= 64 (got %dx%d)",
+                w, h);
+  auto row16 = [](int64_t pitch) { return (pitch * 8) % 16 == 0; };
+  if (!row16(f_pitch) || !row16(pan_pitch) || !al16(pan) || f_pitch < w || pan_pitch < w ||
+      ms_pitch < w / 2 || f_pitch != pan_pitch)
+    return fail(WF_ERR_VALUE, "float64 quality path needs 16-byte aligned rows and one pitch "
+                              "for the fused bands and the PAN");
+  for (int b = 0; b < nbands; ++b) {
+    if (!fused[b] || !ms[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
+    if (!al16(fused[b])) return fail(WF_ERR_VALUE, "band %d not 16-byte aligned", b);
+  }
+  cudaError_t e = wf::launch_quality_scene64(nbands, fused, ms, pan, f_pitch, ms_pitch,
+                                             pan_pitch, h, w, workspace, out, undecidable,
+                                             (cudaStream_t)stream);
+  if (e == cudaSuccess) g_launches += 4;  // scene kernel, edge, two finish levels
+  return cuda_status(e, "wf_quality_scene_f64");
+}
+
 int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
                         int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
                         int w, void* workspace, double* report, int* undecidable, void* stream) {

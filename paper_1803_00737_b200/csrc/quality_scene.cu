@@ -1968,6 +1968,482 @@ __global__ void __launch_bounds__(32 * WF_Q3_WARPS, WF_Q3_MINB)
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// float64 scenes (a reference caller with float64 numpy planes gets float64
+// fused bands, fusion.py:46-47, and qnr() of them): the one-pass report for
+// them, so they no longer fall back to the per-pair kernels (~90 ms per
+// Landsat scene). One warp per 32x32 block (lane = column) marching down a
+// run of block rows with its own cp.async ring of float64 rows; shifts, the
+// bilinear U_k (horizontal then vertical, the reference's order, in float64)
+// and the 2x2 cells (ERGAS, low-resolution D_s moments) in float64; each
+// shifted value x - shift is rounded once to float32 (relative 6e-8) and the
+// 68 second moments accumulate in float32 per lane, float64 across lanes --
+// the same precision as the float32 path. Even lanes score the cells of the
+// first ceil(NB/2) bands, odd lanes the rest (the partner column comes from
+// the staged rows). Per-block partials in the v1/v2 layout (shared finish).
+// ---------------------------------------------------------------------------
+struct QsArgs64 {
+  const double* F[kMaxBandsPerLaunch];
+  const double* M[kMaxBandsPerLaunch];
+  const double* P;
+  long long fp, mp, pp;
+  int H, W, Hh, Wh;
+  int nbr, nbc, nbr_l, nbc_l;
+};
+
+#ifndef WF_Q64_STAGES
+#define WF_Q64_STAGES 5
+#endif
+#ifndef WF_Q64_RUN
+#define WF_Q64_RUN 8
+#endif
+
+template <int NB>
+struct Q64Cfg {
+  static constexpr int S = WF_Q64_STAGES;
+  static constexpr int NPL = NB + 1;
+  static constexpr int MOFF = NPL * 64;            // [plane][row][32] doubles
+  static constexpr int MSEG = 20;                  // [0] = col m0-1, [1..16], [17] = m0+16
+  static constexpr int STAGE = MOFF + NB * MSEG;   // doubles per row-pair stage
+  static constexpr int KH = (NB + 1) / 2;
+  static constexpr int NF = 2 * NB + 1 + 2 * (NB * (NB + 1) / 2) + 2 * NB + 1;
+  static constexpr int NLOW = 3 * NB + 2;
+  static constexpr int NRED = NF + NLOW + 2 * NB;
+  static constexpr int NRED_PAD = (NRED + 31) / 32 * 32;
+};
+
+template <int NB>
+static size_t q64_smem() {
+  using C = Q64Cfg<NB>;
+  return 16 + (size_t)4 * ((size_t)C::S * C::STAGE + C::NRED) * sizeof(double);
+}
+
+__device__ __forceinline__ void cp_async16d(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8d(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128, 2)
+    quality_tile64_kernel(const QsArgs64 a, double* part_q, double* part_low, double* part_erg,
+                          int* undecidable) {
+  using L = QsLayout<NB>;
+  using C = Q64Cfg<NB>;
+  constexpr int S = C::S, KH = C::KH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * S * C::STAGE;
+  double* red = reinterpret_cast<double*>(smem_raw) + (size_t)4 * S * C::STAGE +
+                (size_t)warp * C::NRED;
+  const int runs = (a.nbr + WF_Q64_RUN - 1) / WF_Q64_RUN;
+  const int task = blockIdx.x * 4 + warp;
+  if (task >= runs * a.nbc) return;
+  const int bj = task % a.nbc, run = task / a.nbc;
+  const int bi0 = run * WF_Q64_RUN, bi1 = min(bi0 + WF_Q64_RUN, a.nbr);
+  const int c0 = 32 * bj, m0 = 16 * bj;
+  const int n0 = 16 * bi0, npairs = 16 * (bi1 - bi0);
+  const bool odd = lane & 1;
+
+  // copy roles: plane rows lane >> 4, 16-byte piece lane & 15 (2 doubles);
+  // MS segment column m0 - 1 + lane (lanes < 18, clamped)
+  const long long lane_off = (long long)(lane >> 4) * a.fp + c0 + 2 * (lane & 15);
+  const int lane_dst = (lane >> 4) * 32 + 2 * (lane & 15);
+  const int hcol = min(max(m0 - 1 + lane, 0), a.Wh - 1);
+  int slot_w = 0;
+  auto issue = [&](int t) {
+    if (t < npairs) {
+      double* slot = ring + slot_w * C::STAGE;
+      const long long row = (long long)(2 * (n0 + t)) * a.fp + lane_off;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) cp_async16d(slot + k * 64 + lane_dst, a.F[k] + row);
+      cp_async16d(slot + NB * 64 + lane_dst, a.P + row);
+      const long long mrow = (long long)min(n0 + t + 1, a.Hh - 1) * a.mp + hcol;
+      if (lane < 18) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) cp_async8d(slot + C::MOFF + k * C::MSEG + lane, a.M[k] + mrow);
+      }
+      slot_w = slot_w + 1 == S ? 0 : slot_w + 1;
+    }
+    cp_async_commit();
+  };
+  for (int t = 0; t < S - 1; ++t) issue(t);
+
+  const int ia = (lane + 1) >> 1;  // segment index of x0: even lanes m-1, odd lanes m
+  const double fx = odd ? 0.25 : 0.75;
+  const int xa = min(max(m0 - 1 + ia, 0), a.Wh - 1), xb = min(max(m0 + ia, 0), a.Wh - 1);
+  const int mcol = m0 + (lane >> 1);
+  double hp[NB], hc[NB], mraw[KH];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const double* r0 = a.M[k] + (long long)max(n0 - 1, 0) * a.mp;
+    const double* r1 = a.M[k] + (long long)n0 * a.mp;
+    hp[k] = fma(fx, __ldg(r0 + xb) - __ldg(r0 + xa), __ldg(r0 + xa));
+    hc[k] = fma(fx, __ldg(r1 + xb) - __ldg(r1 + xa), __ldg(r1 + xa));
+  }
+#pragma unroll
+  for (int k = 0; k < KH; ++k) {
+    mraw[k] = 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b == (odd ? KH + k : k)) mraw[k] = __ldg(a.M[b] + (long long)n0 * a.mp + mcol);
+  }
+
+  double kF[NB], kU[NB], kP = 0.0, km[KH], kdp = 0.0;
+  float s1[2 * NB + 1];
+  float2 ffp[NB * (NB + 1) / 4 + NB], uup[NB * (NB + 1) / 4 + NB];
+  float ffs[NB], uus[NB];
+  float2 fu2[(NB + 1) / 2], fp2[(NB + 1) / 2];
+  float pp, l1m[KH], lmm[KH], lmp[KH], l1p, lpp;
+  double sse[KH], summ[KH];
+  auto reset = [&]() {
+#pragma unroll
+    for (int i = 0; i < 2 * NB + 1; ++i) s1[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < NB * (NB + 1) / 4 + NB; ++i) ffp[i] = uup[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) ffs[i] = uus[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < (NB + 1) / 2; ++i) fu2[i] = fp2[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < KH; ++i) {
+      l1m[i] = lmm[i] = lmp[i] = 0.f;
+      sse[i] = summ[i] = 0.0;
+    }
+    pp = l1p = lpp = 0.f;
+  };
+  reset();
+  // one pixel's moments from its float32 shifted values
+  auto moments = [&](const float (&dF0)[NB], const float (&dU0)[NB], float dP) {
+    float dF[NB + 1], dU[NB + 1];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      dF[k] = dF0[k];
+      dU[k] = dU0[k];
+      s1[k] += dF[k];
+      s1[NB + k] += dU[k];
+    }
+    dF[NB] = dU[NB] = 0.f;
+    s1[2 * NB] += dP;
+    int pi = 0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      int l = k;
+      if (k & 1) {
+        ffs[k] = fmaf(dF[k], dF[k], ffs[k]);
+        uus[k] = fmaf(dU[k], dU[k], uus[k]);
+        ++l;
+      }
+      const float2 bf = make_float2(dF[k], dF[k]), bu = make_float2(dU[k], dU[k]);
+#pragma unroll
+      for (; l < NB; l += 2, ++pi) {
+        ffp[pi] = __ffma2_rn(bf, make_float2(dF[l], dF[l + 1]), ffp[pi]);
+        uup[pi] = __ffma2_rn(bu, make_float2(dU[l], dU[l + 1]), uup[pi]);
+      }
+    }
+    const float2 bp = make_float2(dP, dP);
+#pragma unroll
+    for (int k = 0; k < NB; k += 2) {
+      fu2[k / 2] = __ffma2_rn(make_float2(dF[k], dF[k + 1]), make_float2(dU[k], dU[k + 1]),
+                              fu2[k / 2]);
+      fp2[k / 2] = __ffma2_rn(make_float2(dF[k], dF[k + 1]), bp, fp2[k / 2]);
+    }
+    pp = fmaf(dP, dP, pp);
+  };
+
+  int slot_r = 0;
+  for (int t = 0; t < npairs; ++t) {
+    issue(t + S - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const double* st = ring + slot_r * C::STAGE;
+    slot_r = slot_r + 1 == S ? 0 : slot_r + 1;
+    const int tb = t & 15;
+    const int bi = bi0 + (t >> 4);
+    double hn[NB];
+    double mnext[KH];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const double* seg = st + C::MOFF + k * C::MSEG;
+      const double va = seg[ia], vb = seg[ia + 1];
+      hn[k] = fma(fx, vb - va, va);
+    }
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int b = odd ? (KH + k < NB ? KH + k : 0) : k;
+      mnext[k] = st[C::MOFF + b * C::MSEG + 1 + (lane >> 1)];
+    }
+    const bool low_ok = (bi >> 1) < a.nbr_l && (bj >> 1) < a.nbc_l;
+    if (tb == 0) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        kF[k] = __shfl_sync(0xffffffffu, st[k * 64 + lane], 0);
+        kU[k] = __shfl_sync(0xffffffffu, fma(0.75, hc[k] - hp[k], hp[k]), 0);
+      }
+      kP = __shfl_sync(0xffffffffu, st[NB * 64 + lane], 0);
+      const int lr = bi >> 1, lc = min(bj >> 1, max(a.nbc_l - 1, 0));
+      const long long pr = (long long)(64 * lr) * a.pp + 64 * lc;
+      kdp = ((__ldg(a.P + pr) + __ldg(a.P + pr + 1)) +
+             (__ldg(a.P + pr + a.pp) + __ldg(a.P + pr + a.pp + 1))) * 0.25;
+#pragma unroll
+      for (int k = 0; k < KH; ++k) {
+        km[k] = 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b == (odd ? KH + k : k)) km[k] = __ldg(a.M[b] + (long long)(32 * lr) * a.mp + 32 * lc);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {  // rows 2n, 2n+1
+      float dF[NB], dU[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        dF[k] = (float)(st[k * 64 + 32 * r + lane] - kF[k]);
+        const double u = r == 0 ? fma(0.75, hc[k] - hp[k], hp[k])   // MS rows n-1, n
+                                : fma(0.25, hn[k] - hc[k], hc[k]);  // MS rows n, n+1
+        dU[k] = (float)(u - kU[k]);
+      }
+      moments(dF, dU, (float)(st[NB * 64 + 32 * r + lane] - kP));
+    }
+    // cells: ERGAS and the low-resolution D_s moments, this lane's bands
+    const int ce = lane & ~1;
+    const double2 pa = *reinterpret_cast<const double2*>(st + NB * 64 + ce);
+    const double2 pb = *reinterpret_cast<const double2*>(st + NB * 64 + 32 + ce);
+    const double dp = ((pa.x + pa.y) + (pb.x + pb.y)) * 0.25;
+    const float ddp = low_ok ? (float)(dp - kdp) : 0.f;
+    if (!odd) {
+      l1p += ddp;
+      lpp = fmaf(ddp, ddp, lpp);
+    }
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int b = odd ? KH + k : k;
+      if (b < NB) {
+        const double2 fa = *reinterpret_cast<const double2*>(st + b * 64 + ce);
+        const double2 fb = *reinterpret_cast<const double2*>(st + b * 64 + 32 + ce);
+        const double e = ((fa.x + fa.y) + (fb.x + fb.y)) * 0.25 - mraw[k];
+        sse[k] = fma(e, e, sse[k]);
+        summ[k] += mraw[k];
+        const float dm = low_ok ? (float)(mraw[k] - km[k]) : 0.f;
+        l1m[k] += dm;
+        lmm[k] = fmaf(dm, dm, lmm[k]);
+        lmp[k] = fmaf(dm, ddp, lmp[k]);
+      }
+      mraw[k] = mnext[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      hp[k] = hc[k];
+      hc[k] = hn[k];
+    }
+    __syncwarp();
+
+    if (tb == 15) {
+      float v[C::NRED_PAD];
+      int r = 0;
+#pragma unroll
+      for (int i = 0; i < 2 * NB + 1; ++i) v[r++] = s1[i];
+      {
+        int pi = 0;
+        float ff[NB][NB], uu[NB][NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          int l = k;
+          if (k & 1) {
+            ff[k][k] = ffs[k];
+            uu[k][k] = uus[k];
+            ++l;
+          }
+#pragma unroll
+          for (; l < NB; l += 2, ++pi) {
+            ff[k][l] = ffp[pi].x;
+            uu[k][l] = uup[pi].x;
+            if (l + 1 < NB) {
+              ff[k][l + 1] = ffp[pi].y;
+              uu[k][l + 1] = uup[pi].y;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) v[2 * NB + 1 + L::tri(k, l)] = ff[k][l];
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+          for (int l = k; l < NB; ++l) v[2 * NB + 1 + L::NFF + L::tri(k, l)] = uu[k][l];
+        r = 2 * NB + 1 + 2 * L::NFF;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fu2[k / 2].y : fu2[k / 2].x;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v[r++] = (k & 1) ? fp2[k / 2].y : fp2[k / 2].x;
+        v[r++] = pp;
+      }
+      auto band = [&](const float (&x)[KH], int b) -> float {
+        const bool mine = odd ? (b >= KH) : (b < KH);
+        return mine ? x[odd ? (b >= KH ? b - KH : 0) : (b < KH ? b : 0)] : 0.f;
+      };
+#pragma unroll
+      for (int b = 0; b < NB; ++b) v[r++] = band(l1m, b);
+      v[r++] = odd ? 0.f : l1p;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) v[r++] = band(lmm, b);
+      v[r++] = odd ? 0.f : lpp;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) v[r++] = band(lmp, b);
+#pragma unroll
+      for (; r < C::NRED_PAD; ++r) v[r] = 0.f;  // the ERGAS slots go in float64 below
+      constexpr int SSE0 = C::NF + C::NLOW;
+#pragma unroll
+      for (int g = 0; g < C::NRED_PAD / 32; ++g) {
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = v[32 * g + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const float send = up ? x[i] : x[i + o];
+            const float keep = up ? x[i + o] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        const int j = 32 * g + lane;
+        if (j < SSE0) red[j] = (double)x[0];
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const bool mine = odd ? (b >= KH) : (b < KH);
+        const int k = odd ? (b >= KH ? b - KH : 0) : (b < KH ? b : 0);
+        double xs = mine ? sse[k] : 0.0, xm = mine ? summ[k] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          xs += __shfl_xor_sync(0xffffffffu, xs, o);
+          xm += __shfl_xor_sync(0xffffffffu, xm, o);
+        }
+        if (lane == b) {
+          red[SSE0 + b] = xs;
+          red[SSE0 + NB + b] = xm;
+        }
+      }
+      __syncwarp();
+      const size_t blk = (size_t)bi * a.nbc + bj, nparts = (size_t)a.nbr * a.nbc;
+      constexpr int CP = NB * (NB - 1) / 2;
+      const int base2 = 2 * NB + 1;
+      for (int q = lane; q < L::NQ; q += 32) {
+        int pa_, pb_, saa, sbb, sab;
+        if (q < NB) {
+          pa_ = q;
+          pb_ = NB + q;
+          saa = L::tri(q, q);
+          sbb = L::NFF + L::tri(q, q);
+          sab = 2 * L::NFF + q;
+        } else if (q < NB + 2 * CP) {
+          int p = (q - NB) % CP, k = 0;
+          const int off = (q - NB) < CP ? 0 : 1;
+          while (p >= NB - 1 - k) {
+            p -= NB - 1 - k;
+            ++k;
+          }
+          const int l = k + 1 + p;
+          pa_ = off * NB + k;
+          pb_ = off * NB + l;
+          saa = off * L::NFF + L::tri(k, k);
+          sbb = off * L::NFF + L::tri(l, l);
+          sab = off * L::NFF + L::tri(k, l);
+        } else {
+          const int k = q - NB - 2 * CP;
+          pa_ = k;
+          pb_ = 2 * NB;
+          saa = L::tri(k, k);
+          sbb = 2 * L::NFF + 2 * NB;
+          sab = 2 * L::NFF + NB + k;
+        }
+        auto shift = [&](int plane) -> double {
+          double x = kP;
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            if (plane == k) x = kF[k];
+            if (plane == NB + k) x = kU[k];
+          }
+          return x;
+        };
+        part_q[(size_t)q * nparts + blk] =
+            q_from_sums(1024.0, shift(pa_), shift(pb_), red[pa_], red[pb_], red[base2 + saa],
+                        red[base2 + sbb], red[base2 + sab], undecidable);
+      }
+      if (low_ok) {
+        const size_t nlow = (size_t)a.nbr_l * a.nbc_l;
+        double* dst = part_low + (size_t)((bi & 1) * 2 + (bj & 1)) * (L::NLOW + NB + 1) * nlow +
+                      (size_t)((bi >> 1) * a.nbc_l + (bj >> 1));
+        for (int k = lane; k < L::NLOW; k += 32) dst[k * nlow] = red[C::NF + k];
+        if (lane < NB) {
+          double x = 0.0;
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (lane == b) x = __ldg(a.M[b] + (long long)(32 * (bi >> 1)) * a.mp + 32 * (bj >> 1));
+          dst[(L::NLOW + lane) * nlow] = x;
+        }
+        if (lane == 0) dst[(L::NLOW + NB) * nlow] = kdp;
+      }
+      for (int k = lane; k < L::NERG; k += 32) part_erg[k * nparts + blk] = red[SSE0 + k];
+      __syncwarp();
+      reset();
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// ERGAS sums over the MS pixels outside the block grid, float64 planes
+template <int NB>
+__global__ void __launch_bounds__(256)
+    quality_edge64_kernel(const QsArgs64 a, int row_lo, int col_lo, double* part) {
+  __shared__ double redb[2 * NB * 8];
+  const long long n_bottom = (long long)(a.Hh - row_lo) * a.Wh;
+  const long long n_right = (long long)row_lo * (a.Wh - col_lo);
+  const long long n = n_bottom + n_right;
+  double acc[2 * NB];
+#pragma unroll
+  for (int k = 0; k < 2 * NB; ++k) acc[k] = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i, jj;
+    if (e < n_bottom) {
+      i = row_lo + (int)(e / a.Wh);
+      jj = (int)(e % a.Wh);
+    } else {
+      const long long r = e - n_bottom;
+      const int wdt = a.Wh - col_lo;
+      i = (int)(r / wdt);
+      jj = col_lo + (int)(r % wdt);
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const double* f0 = a.F[k] + (long long)(2 * i) * a.fp + 2 * jj;
+      const double d = ((f0[0] + f0[1]) + (f0[a.fp] + f0[a.fp + 1])) * 0.25 -
+                       a.M[k][(long long)i * a.mp + jj];
+      acc[k] += d * d;
+      acc[NB + k] += a.M[k][(long long)i * a.mp + jj];
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 2 * NB; ++k) {
+    const double v = warp_sum_d(acc[k]);
+    if (lane == 0) redb[k * 8 + warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * NB) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += redb[threadIdx.x * 8 + w];
+    part[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+}
+
 // ---- host side ---------------------------------------------------------------
 constexpr int kEdgeCtas = 256;
 
@@ -2227,6 +2703,80 @@ cudaError_t launch_fuse_quality_haar(int nb, const float* P, const float* const*
     return launch_qs_nb<N>(nullptr, M, P, op, mp, pp, h, w, workspace, out, undecidable, s, O);
     WF_FQ(2) WF_FQ(3) WF_FQ(4) WF_FQ(5) WF_FQ(6) WF_FQ(7) WF_FQ(8)
 #undef WF_FQ
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int NB>
+static cudaError_t launch_qs64_nb(const double* const* F, const double* const* M, const double* P,
+                                  long long fp, long long mp, long long pp, int h, int w,
+                                  void* workspace, double* out, int* undecidable,
+                                  cudaStream_t s) {
+  using L = QsLayout<NB>;
+  QsArgs64 a{};
+  for (int k = 0; k < NB; ++k) {
+    a.F[k] = F[k];
+    a.M[k] = M[k];
+  }
+  a.P = P;
+  a.fp = fp;
+  a.mp = mp;
+  a.pp = pp;
+  a.H = h;
+  a.W = w;
+  a.Hh = h / 2;
+  a.Wh = w / 2;
+  int ncx = 0;
+  qs_geometry(h, w, a.nbr, a.nbc, a.nbr_l, a.nbc_l, ncx, 1);
+  QsArgs ad{};  // the grid, for the shared finish kernels
+  ad.H = h;
+  ad.W = w;
+  ad.Hh = h / 2;
+  ad.Wh = w / 2;
+  ad.nbr = a.nbr;
+  ad.nbc = a.nbc;
+  ad.nbr_l = a.nbr_l;
+  ad.nbc_l = a.nbc_l;
+  const int nparts = a.nbr * a.nbc;
+  double* pq = static_cast<double*>(workspace);
+  double* pl = pq + (size_t)nparts * L::NQ;
+  double* pe = pl + (size_t)a.nbr_l * a.nbc_l * 4 * (L::NLOW + NB + 1);
+  double* pg = pe + (size_t)nparts * L::NERG;
+  double* fin = pg + (size_t)kEdgeCtas * 2 * NB;
+  const size_t smem = q64_smem<NB>();
+  cudaError_t e = cudaFuncSetAttribute(quality_tile64_kernel<NB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(undecidable, 0, sizeof(int), s)) != cudaSuccess) return e;
+  const int runs = (a.nbr + WF_Q64_RUN - 1) / WF_Q64_RUN;
+  const int ctas = (runs * a.nbc + 3) / 4;
+  if (ctas > 0)
+    quality_tile64_kernel<NB><<<ctas, 128, smem, s>>>(a, pq, pl, pe, undecidable);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int row_lo = 16 * a.nbr, col_lo = 16 * a.nbc;
+  int nedge = 0;
+  if (row_lo < a.Hh || col_lo < a.Wh) {
+    nedge = kEdgeCtas;
+    quality_edge64_kernel<NB><<<nedge, 256, 0, s>>>(a, row_lo, col_lo, pg);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  quality_finish_kernel<NB><<<dim3(L::NQ + 3 * NB, kFinSplit), kFinThreads, 0, s>>>(
+      ad, pq, nparts, pl, pe, pg, nedge, fin, undecidable);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  quality_finish2_kernel<NB><<<1, 128, 0, s>>>(ad, fin, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quality_scene64(int nb, const double* const* F, const double* const* M,
+                                   const double* P, long long fp, long long mp, long long pp,
+                                   int h, int w, void* workspace, double* out, int* undecidable,
+                                   cudaStream_t s) {
+  switch (nb) {
+#define WF_Q64(N) \
+  case N:         \
+    return launch_qs64_nb<N>(F, M, P, fp, mp, pp, h, w, workspace, out, undecidable, s);
+    WF_Q64(2) WF_Q64(3) WF_Q64(4) WF_Q64(5) WF_Q64(6) WF_Q64(7) WF_Q64(8)
+#undef WF_Q64
     default: return cudaErrorInvalidValue;
   }
 }

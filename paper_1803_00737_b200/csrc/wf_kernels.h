@@ -137,6 +137,10 @@ cudaError_t launch_fuse_quality_haar(int nb, const float* P, const float* const*
                                      float* const* O, long long op, long long mp, long long pp,
                                      int h, int w, void* workspace, double* out,
                                      int* undecidable, cudaStream_t s);
+cudaError_t launch_quality_scene64(int nb, const double* const* F, const double* const* M,
+                                   const double* P, long long fp, long long mp, long long pp,
+                                   int h, int w, void* workspace, double* out, int* undecidable,
+                                   cudaStream_t s);
 cudaError_t launch_quality_scene(int nb, const float* const* F, const float* const* M,
                                  const float* P, long long fp, long long mp, long long pp, int h,
                                  int w, void* workspace, double* out, int* undecidable,

@@ -264,21 +264,28 @@ def d_s(fused, ms, pan) -> float:
     return _ds_value(res.host(), pairs)
 
 
-def _qnr_scene(f_t, m_t, p_t, ratio) -> QualityReport | None:
-    """One-pass fused report (csrc/quality_scene.cu) when the scene qualifies:
-    float32 planes, ratio 2, 2..8 bands, H, W >= 64. None = use the generic
-    path (also when a block needs the element-wise identity test)."""
-    n = len(f_t)
-    h, w = p_t.shape
-    if not _scene_ok((*f_t, *m_t, p_t), n, h, w, ratio):
-        return None
+def _scene_launch(f_t, m_t, p_t, n, h, w, ws, out, flag) -> None:
+    """wf_quality_scene_f32, or wf_quality_scene_f64 for float64 scenes."""
     lib = _native.load()
-    ws, out, flag = _scene_buffers(n, h, w, p_t.device)
-    _native.check(lib.wf_quality_scene_f32(
+    fn = lib.wf_quality_scene_f32 if p_t.dtype == torch.float32 else lib.wf_quality_scene_f64
+    _native.check(fn(
         _native.ptr_array([t.data_ptr() for t in f_t]),
         _native.ptr_array([t.data_ptr() for t in m_t]), p_t.data_ptr(), f_t[0].stride(0),
         m_t[0].stride(0), p_t.stride(0), n, h, w, ws.data_ptr(), out.data_ptr(),
         flag.data_ptr(), _device.stream_ptr()))
+
+
+def _qnr_scene(f_t, m_t, p_t, ratio) -> QualityReport | None:
+    """One-pass fused report (csrc/quality_scene.cu) when the scene qualifies:
+    float32 or float64 planes (all one dtype), ratio 2, 2..8 bands, H, W >= 64.
+    None = use the generic path (also when a block needs the element-wise
+    identity test)."""
+    n = len(f_t)
+    h, w = p_t.shape
+    if not _scene_ok((*f_t, *m_t, p_t), n, h, w, ratio):
+        return None
+    ws, out, flag = _scene_buffers(n, h, w, p_t.device)
+    _scene_launch(f_t, m_t, p_t, n, h, w, ws, out, flag)
     if int(flag.item()):
         return None
     return _scene_report(out.cpu().numpy(), n, ratio)
@@ -287,10 +294,14 @@ def _qnr_scene(f_t, m_t, p_t, ratio) -> QualityReport | None:
 def _scene_ok(tensors, n, h, w, ratio) -> bool:
     import os
 
-    return not (os.environ.get("WF_QNR_PATH") == "generic" or ratio != 2 or not 2 <= n <= 8
-                or h < 64 or w < 64 or w % 8
-                or any(t.dtype != torch.float32 for t in tensors)
-                or any(t.data_ptr() % 16 for t in tensors))
+    dt = tensors[-1].dtype
+    if os.environ.get("WF_QNR_PATH") == "generic" or ratio != 2 or not 2 <= n <= 8 \
+            or h < 64 or w < 64 or w % 8 or dt not in (torch.float32, torch.float64) \
+            or any(t.dtype != dt for t in tensors) or any(t.data_ptr() % 16 for t in tensors):
+        return False
+    # float64: the fused bands and the PAN share one pitch (16-byte rows)
+    return dt == torch.float32 or (all(t.stride(0) == tensors[-1].stride(0)
+                                       for t in tensors[:n]) and tensors[-1].stride(0) % 2 == 0)
 
 
 def _scene_buffers(n, h, w, device):
@@ -372,13 +383,8 @@ def qnr_async(fused, ms, pan) -> PendingReport:
     h, w = p_t.shape
     if not _scene_ok((*f_t, *m_t, p_t), n, h, w, ratio):
         return PendingReport((fused, ms, pan), None, n, ratio)
-    lib = _native.load()
     ws, out, flag = _scene_buffers(n, h, w, p_t.device)
-    _native.check(lib.wf_quality_scene_f32(
-        _native.ptr_array([t.data_ptr() for t in f_t]),
-        _native.ptr_array([t.data_ptr() for t in m_t]), p_t.data_ptr(), f_t[0].stride(0),
-        m_t[0].stride(0), p_t.stride(0), n, h, w, ws.data_ptr(), out.data_ptr(),
-        flag.data_ptr(), _device.stream_ptr()))
+    _scene_launch(f_t, m_t, p_t, n, h, w, ws, out, flag)
     # the workspace goes back to the caching allocator now: any later user of
     # that memory is ordered after these kernels on the same stream
     del ws
