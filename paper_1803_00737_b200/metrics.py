@@ -349,6 +349,10 @@ class PendingReport:
     def __init__(self, args, bufs, n, ratio):
         self._args, self._bufs, self._n, self._ratio = args, bufs, n, ratio
         self._report = None
+        self._done = None
+        if bufs is not None:  # result() may run on another stream than the kernels
+            self._done = torch.cuda.Event()
+            self._done.record(torch.cuda.current_stream())
 
     def result(self) -> QualityReport:
         if self._report is None:
@@ -356,6 +360,7 @@ class PendingReport:
                 self._report = qnr(*self._args)
             else:
                 _, out, flag = self._bufs
+                torch.cuda.current_stream().wait_event(self._done)
                 vals = torch.cat([out, flag.to(torch.float64)]).cpu().numpy()
                 if int(vals[-1]):
                     self._report = qnr(*self._args)

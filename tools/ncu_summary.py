@@ -31,8 +31,14 @@ def _key(short: str) -> str:
     if short.startswith("quality_split_kernel<"):  # <NB, FUSE>: bench.py reads quality_split_kernel_6
         nb, *fuse = [t.strip() for t in short.split("<")[1].rstrip(">").split(",")]
         return "quality_split_kernel_" + nb + ("_fused" if fuse and fuse[0] not in ("0", "false") else "")
-    if short.startswith("fuse_d4_u8x8_kernel<"):
-        return "fuse_d4_u8x8_kernel_" + short.split("<")[1].split(",")[0].strip()
+    if short.startswith("fuse_d4_u8x8_kernel<"):  # <NB, NCW, MINB, CVT, EXACT>: v3 = EXACT
+        args = [t.strip() for t in short.split("<")[1].rstrip(">").split(",")]
+        v2 = len(args) > 4 and args[4] in ("0", "false")
+        return "fuse_d4_u8x8_kernel_" + args[0] + ("_v2" if v2 else "")
+    if short.startswith("quality_tile64_kernel<"):
+        return "quality_tile64_kernel_" + short.split("<")[1].rstrip(">").strip()
+    if short.startswith("quality_tile_kernel<"):
+        return "quality_tile_kernel_" + short.split("<")[1].rstrip(">").strip()
     return "".join(c if c.isalnum() else "_" for c in short.replace("wf::", "")).strip("_")
 
 
