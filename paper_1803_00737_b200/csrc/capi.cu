@@ -201,6 +201,8 @@ int fuse_common(int kind, const T* pan, int64_t pan_pitch, const T* pan_top, con
     cudaError_t e = wf::launch_fuse<T, Acc>(kind, a, vec, tma, s, tune);
     if (e != cudaSuccess) return cuda_status(e, "fuse launch");
     ++g_launches;
+    // the byte-exact 8 bpp D4 kernel is followed by its fix-up kernel
+    if (sizeof(T) == 1 && kind == WF_DAUB4 && tune.d4_u8_variant == 0) ++g_launches;
   }
   return WF_OK;
 }

@@ -420,19 +420,20 @@ __device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, boo
 // reference's byte differ. Such pixels are detected two per instruction
 // (PRMT the fraction byte above the low integer byte; the 16-bit lane is then
 // < 256 exactly when the fraction byte is 0; VIMNMX3.U16x2 keeps the minimum),
-// and the thread's 2 x 8-pixel unit of that band is queued in a per-warp
-// shared-memory list (0.4% of pixels, ~6% of units). At the end of its row
-// run a warp recomputes them -- one unit per lane, PAN/MS re-read through L2
-// (the CTA just bulk-copied them) -- in float64 (fix_unit_u8), and rewrites their
+// and the thread's 2 x 8-pixel unit of that band is appended to its warp's
+// list in global memory (0.4% of pixels, ~6% of units). A second kernel
+// (fix_u8_kernel, one warp per list, thousands of warps in flight) recomputes
+// them -- one unit per lane -- in float64 (fix_unit_u8), and rewrites their
 // 16 bytes: a float64 value further than 1e-9 from every byte boundary of
 // the float32 cast gives the reference's byte outright (float64 evaluation
 // orders differ by << 1e-9 here); a closer one is recomputed in the
 // reference's own float64 operation order (ref_pixel_u8). The other 99.6% of
 // pixels keep the float32 byte, which is provably the reference's.
 // ---------------------------------------------------------------------------
-// queued units per warp and task: 16 row pairs x 32 lanes x NB bands x ~6% flagged
-// = ~184 expected at 6 bands; an overflow re-does the warp's whole run
-constexpr int kU8FixCap = 512;
+// list capacity per (task, warp): 16 row pairs x 32 lanes x NB bands x ~6%
+// flagged = ~31 NB expected; 32 NB + 96 is >= 5 sigma above that for every NB.
+// An overflowing list re-does the warp's whole run.
+__host__ __device__ constexpr int u8_fix_cap(int nb) { return 32 * nb + 96; }
 
 __device__ __forceinline__ uint32_t quantize_ref(float f) {  // imageio.py:115-123 in float32
   const float c = fminf(fmaxf(f, 0.0f), 255.0f);
@@ -683,10 +684,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   // conflict-free), not in 5*NB registers: registers then fit 4 CTAs per SM
   float4* ep4 = reinterpret_cast<float4*>(empty + S) + t;  // [NB][NCW*32]
   float* ep1 = reinterpret_cast<float*>(reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + t;
-  // EXACT: this warp's queue of units to recompute (after the carry arrays)
-  uint32_t* fixq = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(
-                       reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + NB * NCW * 32) +
-                   warp * kU8FixCap;
+  // EXACT: this warp's list of units to recompute (global memory)
+  uint32_t* fixq = EXACT ? a.fixq + ((size_t)blockIdx.x * NCW + warp) * a.fixcap : nullptr;
   int fixn = 0;  // queued units (warp-uniform)
 
   // v2 unrolls the row-pair loop twice; v3's longer body is not unrolled (two
@@ -786,7 +785,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, flag);
             if (bal) {  // warp-uniform
               const int pos = fixn + __popc(bal & ((1u << lane) - 1u));
-              if (flag && pos < kU8FixCap)
+              if (flag && pos < a.fixcap)
                 fixq[pos] = ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b;
               fixn += __popc(bal);
             }
@@ -839,24 +838,40 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
     if (lane == 0) tma::mbar_arrive(&empty[s]);
   }
   if constexpr (EXACT) {
-    // The warp's queued units, recomputed in float64 once its row run is
-    // done (the loop above holds no state across this, so the fix-up's
-    // registers cost the streaming loop nothing; the task's rows are still
-    // in L2). The bytes were stored by this warp's lanes in the loop;
-    // __syncwarp orders those stores and the queue writes before the rewrites.
-    __syncwarp();
-    if (a.fix_mode == 3) return;  // timing experiment: detection only
-    // queued units, one per lane in turn; after a queue overflow (inputs with
-    // many values at rounding boundaries) every unit of this lane's column
-    // group instead, all row pairs and bands (one inlined copy of the fix-up)
-    const bool over = fixn > kU8FixCap;
-    const int cnt = over ? (valid ? (i1 - i0) * NB : 0) : (fixn - lane + 31) / 32;
-    for (int k = 0; k < cnt; ++k) {
-      const uint32_t e = over ? ((uint32_t)(i0 + k / NB) << 11) | ((uint32_t)t << 4) |
-                                    (uint32_t)(k % NB)
-                              : fixq[lane + 32 * k];
-      fix_entry_u8<NB>(a, e, base);
-    }
+    if (lane == 0) a.fixn[(size_t)blockIdx.x * NCW + warp] = fixn;
+  }
+}
+
+// The 8 bpp D4 fix-up: one warp per (task, consumer warp) list of
+// fuse_d4_u8x8_kernel<..., EXACT>, one queued unit per lane in turn (the
+// lists' entries and bytes were written by the previous kernel on the same
+// stream). An overflowing list (inputs with many values at rounding
+// boundaries) re-does every unit of that warp's column group and row run.
+template <int NB, int NCW>
+__global__ void __launch_bounds__(32 * NCW)
+    fix_u8_kernel(const FuseArgs<uint8_t> a) {
+  if (a.fix_mode == 3) return;  // timing experiment: detection only
+  constexpr int CW = 256 * NCW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb = (int)(blockIdx.x % (unsigned)a.n_colbands);
+  const int rt = (int)(blockIdx.x / (unsigned)a.n_colbands);
+  const int base = cb * CW;
+  const int len = min(CW, a.W - base);
+  const int npairs = a.rows >> 1;
+  const int i0 = rt * a.pairs_per_task;
+  const int i1 = min(i0 + a.pairs_per_task, npairs);
+  const int t = warp * 32 + lane;
+  const bool valid = 8 * t < len;
+  const size_t list = (size_t)blockIdx.x * NCW + warp;
+  const int fixn = a.fixn[list];
+  const uint32_t* fixq = a.fixq + list * a.fixcap;
+  const bool over = fixn > a.fixcap;
+  const int cnt = over ? (valid ? (i1 - i0) * NB : 0) : (fixn - lane + 31) / 32;
+  for (int k = 0; k < cnt; ++k) {
+    const uint32_t e = over ? ((uint32_t)(i0 + k / NB) << 11) | ((uint32_t)t << 4) |
+                                  (uint32_t)(k % NB)
+                            : fixq[lane + 32 * k];
+    fix_entry_u8<NB>(a, e, base);
   }
 }
 
@@ -870,11 +885,9 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   int S = tune.d4_stages > 0 ? tune.d4_stages : (int)((32 * 1024) / SLOT);
   if (S < 2) S = 2;
   if (S > 16) S = 16;
-  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer
-  // thread) + (EXACT) the per-warp fix-up queues
+  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer thread)
   const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
-                      (size_t)NB * NCW * 32 * 20 +
-                      (EXACT ? (size_t)NCW * kU8FixCap * sizeof(uint32_t) : 0);
+                      (size_t)NB * NCW * 32 * 20;
   a.fix_mode = EXACT ? tune.u8_fix_mode : 0;
   auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT, EXACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -887,8 +900,28 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;
   a.n_tasks = n_row * a.n_colbands;
+  void* scratch = nullptr;
+  if constexpr (EXACT) {
+    // the fix-up lists, stream-ordered (re-entrant: one allocation per call)
+    a.fixcap = u8_fix_cap(NB);
+    const size_t lists = (size_t)a.n_tasks * NCW;
+    if ((e = cudaMallocAsync(&scratch, lists * ((size_t)a.fixcap + 1) * sizeof(uint32_t), s)) !=
+        cudaSuccess)
+      return e;
+    a.fixn = static_cast<int*>(scratch);
+    a.fixq = reinterpret_cast<uint32_t*>(a.fixn + lists);
+  }
   kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if constexpr (EXACT) {
+    if (e == cudaSuccess) {
+      fix_u8_kernel<NB, NCW><<<(unsigned)a.n_tasks, 32 * NCW, 0, s>>>(a);
+      e = cudaGetLastError();
+    }
+    const cudaError_t f = cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 template <bool EXACT>

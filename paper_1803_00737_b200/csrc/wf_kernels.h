@@ -29,6 +29,9 @@ struct FuseArgs {
   int nbands;
   int wide;  // float64 with 32-byte aligned rows: 256-bit PAN loads / output stores
   int fix_mode;  // 8 bpp D4 v3: 0 normal, 1 every unit re-done in float64, 2 in reference order
+  uint32_t* fixq;  // 8 bpp D4 v3: per (task, consumer warp) list of units to recompute
+  int* fixn;       //   and its length (> capacity: overflow, re-do the warp's whole run)
+  int fixcap;      //   entries per list
   int rows;  // PAN rows in this launch (even)
   int W;     // PAN columns (even)
   // filled by the launcher

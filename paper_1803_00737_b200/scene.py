@@ -71,60 +71,3 @@ class DeviceScene:
 
         return run
 
-
-class FuseScorePipeline:
-    """Fusion and the QNR/ERGAS report of a sequence of scenes on two CUDA
-    streams (the C5 batch): scene k's report (issue-bound,
-    about half the HBM bandwidth) runs while scene k+1 fuses (HBM-bound, few
-    issue slots), on two output sets used in turn. Each submit() queues one
-    fusion launch and one report; the reports' scalars are read later, once,
-    through the returned PendingReport (metrics.qnr_async), so the GPU never
-    idles on a host sync. Same kernels and results as fuse() then qnr().
-
-    Stream order: the fusion into output set k % 2 waits for the report that
-    last read that set; the report waits for its fusion. wait() makes the
-    caller's current stream wait for everything submitted."""
-
-    def __init__(self, shape, bands: int, device=None):
-        dev = _device.require_cuda() if device is None else device
-        h, w = shape
-        self.outs = [[torch.empty((h, w), dtype=torch.float32, device=dev) for _ in range(bands)]
-                     for _ in range(2)]
-        self.s_fuse = torch.cuda.Stream(device=dev)
-        self.s_score = torch.cuda.Stream(device=dev)
-        self.fused = [torch.cuda.Event(), torch.cuda.Event()]
-        self.scored = [torch.cuda.Event(), torch.cuda.Event()]
-        self.k = 0
-        self.started = False
-
-    def submit(self, scene: "DeviceScene", kind: WaveletKind):
-        from .metrics import qnr_async
-
-        if not self.started:  # nothing before this point on the caller's stream is skipped
-            cur = torch.cuda.current_stream()
-            self.s_fuse.wait_stream(cur)
-            self.s_score.wait_stream(cur)
-            self.started = True
-        slot = self.k % 2
-        outs = self.outs[slot]
-        lib = _native.load()
-        h, w = scene.shape
-        self.s_fuse.wait_event(self.scored[slot])
-        _native.check(lib.wf_fuse_bands_f32(
-            KIND_CODE[kind], scene.pan.data_ptr(), w,
-            _native.ptr_array([m.data_ptr() for m in scene.ms]), w // 2,
-            _native.ptr_array([o.data_ptr() for o in outs]), w, len(scene.ms), h, w,
-            self.s_fuse.cuda_stream))
-        self.fused[slot].record(self.s_fuse)
-        self.s_score.wait_event(self.fused[slot])
-        with torch.cuda.stream(self.s_score):
-            pending = qnr_async(outs, scene.ms, scene.pan)
-        self.scored[slot].record(self.s_score)
-        self.k += 1
-        return pending
-
-    def wait(self) -> None:
-        cur = torch.cuda.current_stream()
-        cur.wait_stream(self.s_fuse)
-        cur.wait_stream(self.s_score)
-        self.started = False
