@@ -914,28 +914,57 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;
   a.n_tasks = n_row * a.n_colbands;
-  void* scratch = nullptr;
-  if constexpr (EXACT) {
+  if constexpr (!EXACT) {
+    kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
+    return cudaGetLastError();
+  } else {
+    // WF_U8_CHUNK_PAIRS (experiment): row chunks (whole-plane launches only:
+    // a chunk's halo rows are its neighbours' rows of the same plane), each
+    // streaming kernel followed by its fix-up kernel, so that the fix-up
+    // re-reads rows the chunk has just pulled through L2. Measured slower on
+    // the Landsat scene (one-wave chunks 1.58 ms, 2368-row chunks 1.36 ms,
+    // unchunked 1.06 ms; profiles/r02_u8_fixup_timing.log): the per-chunk
+    // ramps cost more than the re-reads.
+    long long chunk_pairs = tune.u8_chunk_pairs > 0 ? tune.u8_chunk_pairs : npairs;
+    const bool chunked = a.halo_pitch == a.pan_pitch && npairs > 2 * chunk_pairs;
+    if (!chunked) chunk_pairs = npairs;
+    const long long tasks_max = ((chunk_pairs + P - 1) / P) * a.n_colbands;
     // the fix-up lists, stream-ordered (re-entrant: one allocation per call)
     a.fixcap = u8_fix_cap(NB);
-    const size_t lists = (size_t)a.n_tasks * NCW;
+    const size_t lists = (size_t)tasks_max * NCW;
+    void* scratch = nullptr;
     if ((e = cudaMallocAsync(&scratch, lists * ((size_t)a.fixcap + 1) * sizeof(uint32_t), s)) !=
         cudaSuccess)
       return e;
     a.fixn = static_cast<int*>(scratch);
     a.fixq = reinterpret_cast<uint32_t*>(a.fixn + lists);
-  }
-  kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
-  e = cudaGetLastError();
-  if constexpr (EXACT) {
-    if (e == cudaSuccess) {
-      fix_u8_kernel<NB, NCW><<<(unsigned)a.n_tasks, 32 * NCW, 0, s>>>(a);
+    for (long long p0 = 0; p0 < npairs && e == cudaSuccess; p0 += chunk_pairs) {
+      const long long np = npairs - p0 < chunk_pairs ? npairs - p0 : chunk_pairs;
+      FuseArgs<uint8_t> c = a;
+      if (chunked) {
+        const long long r0 = 2 * p0, r1 = 2 * (p0 + np);
+        c.pan = a.pan + r0 * a.pan_pitch;
+        c.rows = (int)(r1 - r0);
+        c.pan_top = p0 == 0 ? a.pan_top : a.pan + (r0 - 2) * a.pan_pitch;
+        c.pan_bot = p0 + np == npairs ? a.pan_bot : a.pan + r1 * a.pan_pitch;
+        for (int b = 0; b < a.nbands; ++b) {
+          c.ms[b] = a.ms[b] + p0 * a.ms_pitch;
+          c.ms_top[b] = p0 == 0 ? a.ms_top[b] : a.ms[b] + (p0 - 1) * a.ms_pitch;
+          c.out[b] = a.out[b] + r0 * a.out_pitch;
+        }
+        c.n_tasks = ((np + P - 1) / P) * a.n_colbands;
+      }
+      kern<<<(unsigned)c.n_tasks, 32 * (NCW + 1), smem, s>>>(c, S);
       e = cudaGetLastError();
+      if (e == cudaSuccess) {
+        fix_u8_kernel<NB, NCW><<<(unsigned)c.n_tasks, 32 * NCW, 0, s>>>(c);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) count_extra_launches(p0 == 0 ? 1 : 2);
     }
     const cudaError_t f = cudaFreeAsync(scratch, s);
-    if (e == cudaSuccess) e = f;
+    return e == cudaSuccess ? f : e;
   }
-  return e;
 }
 
 template <bool EXACT>

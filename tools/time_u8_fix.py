@@ -20,9 +20,13 @@ del sc
 lib = _native.load()
 mp = _native.ptr_array([m.data_ptr() for m in ms])
 res = {}
-for variant, fix in (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", "")):
+chunks = sys.argv[1:] or ["0"]  # WF_U8_CHUNK_PAIRS values for the full v3 pair (0 = auto)
+cases = [("v3", "", ch) for ch in chunks] + [("v3", "skipfix", "0"), ("v3", "nodetect", "0"),
+                                            ("v2", "", "0")]
+for variant, fix, ch in cases:
     os.environ["WF_D4_U8"] = variant
     os.environ["WF_U8_FIX"] = fix
+    os.environ["WF_U8_CHUNK_PAIRS"] = ch
     _native.reload_tuning()
     out = [torch.empty((H, W), dtype=torch.uint8, device="cuda") for _ in ms]
     op = _native.ptr_array([o.data_ptr() for o in out])
@@ -37,7 +41,8 @@ for variant, fix in (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", "
         run()
     e1.record()
     torch.cuda.synchronize()
-    print(f"{variant} {fix or 'full'}: {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
+    print(f"{variant} {fix or 'full'} chunk_pairs={ch}: {e0.elapsed_time(e1) / 10:.3f} ms",
+          flush=True)
     res[(variant, fix)] = out
 full, skip = res[("v3", "")], res[("v3", "skipfix")]
 changed = sum(int((a != b).sum()) for a, b in zip(full, skip))
