@@ -56,6 +56,12 @@ PAPER_HDWT_MPIX = 67.5  # BASELINE.md section 1 (paper, HDWT, 16280x14960)
 PAPER_DDWT_MPIX = 65.8
 
 
+def landsat_config(world: int) -> dict:
+    """The workload both arms report (configs[1]/[2]: one Landsat-shaped
+    scene per GPU); implementation details go under "execution"."""
+    return {"workload": WORKLOAD, "global_batch": world, "bands": B}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,8 +248,12 @@ def run_reference(args, rank: int):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (counter-hash uniform[0,255) f32)",
-        "config": {"workload": WORKLOAD, "global_batch": 1, "sample_rows": args.cpu_rows,
-                   "parallelism": f"{threads} host threads"},
+        # the same config dict as our arm's (the driver compares them); how the
+        # CPU arm runs it goes under "execution"
+        "config": landsat_config(args.gpus),
+        "execution": {"sample_rows": args.cpu_rows, "parallelism": f"{threads} host threads",
+                      "per_pixel_rate": "the scene-MPix/s of a bounded row sample (a rate, so "
+                                        "no extrapolation)"},
         "cpu_baseline": {"value": round(rate, 3), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -868,10 +878,8 @@ def run_ours(args, rank, world, local_rank):
                                    "source": "BASELINE.md s1 / PAPER.md:153-156 (HDWT, GTX 460 x4)"},
             "dtype": "f32",
             "data": "synthetic (device counter-hash uniform[0,255) f32, Landsat-7-shaped)",
-            "config": {
-                "workload": WORKLOAD,
-                "global_batch": world,
-                "bands": B,
+            "config": landsat_config(world),
+            "execution": {
                 "parallelism": f"scene-sharded replicas x{world} (no collective)",
                 "l2": "no flush: 2.24 GB of inputs per step >> 126 MB L2",
                 "host_cpus": _BOUND.get("cpus"),
