@@ -41,7 +41,6 @@ static LaunchTuning read_tuning() {
   v.d4_stages = num("WF_D4_STAGES");
   v.haar_u8_ppt = num("WF_HAAR_U8_PPT");
   v.d4_u8_variant = is("WF_D4_U8", "v1") ? 1 : is("WF_D4_U8", "v2") ? 2 : 0;
-  v.u8_chunk_pairs = num("WF_U8_CHUNK_PAIRS");
   v.u8_fix_mode = is("WF_U8_FIX", "all")       ? 1
                   : is("WF_U8_FIX", "ref")     ? 2
                   : is("WF_U8_FIX", "skipfix") ? 3   // timing experiments only:
@@ -56,9 +55,7 @@ static LaunchTuning read_tuning() {
   return v;
 }
 static LaunchTuning g_tuning = read_tuning();
-// launchers that issue more than the one kernel per call the C ABI counts
-// report the extra ones here (wf_launch_count)
-void count_extra_launches(int n);
+
 const LaunchTuning& env_tuning() { return g_tuning; }
 }  // namespace wf
 
@@ -563,10 +560,6 @@ int fuse_host_impl(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* c
 }
 
 }  // namespace
-
-namespace wf {
-void count_extra_launches(int n) { g_launches += n; }
-}  // namespace wf
 
 extern "C" {
 

@@ -385,6 +385,9 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
 #ifndef WF_U8X8_MIN_CTAS
 #define WF_U8X8_MIN_CTAS 4
 #endif
+#ifndef WF_U8X8E_MIN_CTAS  // the byte-exact variant: the in-ring fix-up needs registers
+#define WF_U8X8E_MIN_CTAS 3
+#endif
 
 // byte `byte` of w as a float. ALU = false: I2F.U8 with a byte select (XU
 // pipe, quarter rate); ALU = true: PRMT zero-extend + I2FP.F32.U32 (ALU pipe),
@@ -421,20 +424,16 @@ __device__ __forceinline__ void st_cs_v2_if(void* p, uint32_t x, uint32_t y, boo
 // (PRMT the fraction byte above the low integer byte; the 16-bit lane is then
 // < 256 exactly when the fraction byte is 0; VIMNMX3.U16x2 keeps the minimum),
 // and the thread's 2 x 8-pixel unit of that band is appended to its warp's
-// list in global memory (0.4% of pixels, ~6% of units). A second kernel
-// (fix_u8_kernel, one warp per list, thousands of warps in flight) recomputes
-// them -- one unit per lane -- in float64 (fix_unit_u8), and rewrites their
-// 16 bytes: a float64 value further than 1e-9 from every byte boundary of
-// the float32 cast gives the reference's byte outright (float64 evaluation
-// orders differ by << 1e-9 here); a closer one is recomputed in the
+// queue in shared memory (0.4% of pixels, ~6% of units). Every second row
+// pair the CTA's consumer threads recompute the queued units -- one per
+// thread, the PAN/MS rows read from the ring, whose slots are released three
+// row pairs late for this -- in float64 (fix_unit_ring / fix_unit_core), and
+// rewrite their 16 bytes: a float64 value further than 1e-9 from every byte
+// boundary of the float32 cast gives the reference's byte outright (float64
+// evaluation orders differ by << 1e-9 here); a closer one is recomputed in the
 // reference's own float64 operation order (ref_pixel_u8). The other 99.6% of
 // pixels keep the float32 byte, which is provably the reference's.
 // ---------------------------------------------------------------------------
-// list capacity per (task, warp): 16 row pairs x 32 lanes x NB bands x ~6%
-// flagged = ~31 NB expected; 32 NB + 96 is >= 5 sigma above that for every NB.
-// An overflowing list re-does the warp's whole run.
-__host__ __device__ constexpr int u8_fix_cap(int nb) { return 32 * nb + 96; }
-
 __device__ __forceinline__ uint32_t quantize_ref(float f) {  // imageio.py:115-123 in float32
   const float c = fminf(fmaxf(f, 0.0f), 255.0f);
   return (uint32_t)floorf(__fadd_rn(c, 0.5f));
@@ -541,47 +540,15 @@ __device__ __forceinline__ double byte_at2(const uint32_t (&w)[2], int k) {
 }
 
 // Recompute the queued unit (row pair i, first column c: output rows 2i,
-// 2i+1 x columns c .. c+7) in float64 and store its 16 bytes. fix_mode 2
-// (test hook): every pixel takes the reference-order path. Inlined into the
-// kernel's tail (after the streaming loop, whose registers are dead there):
-// as a called function its frame and spills went to local memory, and with
-// the shared-memory carve-out leaving ~30 KB of L1 those round-trips ran at
-// L2 latency.
-__device__ __forceinline__ void fix_unit_u8(const U8Band& u, int i, int c) {
-  const int W = u.W, Wh = W >> 1, j = c >> 1;
+// 2i+1 x columns c .. c+7) in float64 from its PAN words w[k] (rows 2i-2+k,
+// bytes = columns c-4 .. c+11) and MS words mw[k] (rows i-1+k, half-columns
+// j-4 .. j+3), and store its 16 bytes. fix_mode 2 (test hook): every pixel
+// takes the reference-order path.
+__device__ __forceinline__ void fix_unit_core(const U8Band& u, int i, int c,
+                                              const uint32_t (&w)[6][4],
+                                              const uint32_t (&mw)[2][2]) {
   const D4 tp = d4_taps();
   const double h0 = tp.h0, h1 = tp.h1, h2 = tp.h2, h3 = tp.h3;
-  // MS rows i-1, i: bytes of half-columns j-4 .. j+3 (periodic in the window)
-  uint32_t mw[2][2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const uint8_t* row = u.ms_row(i - 1 + k);
-    if (j >= 4 && j + 4 <= Wh) {
-      mw[k][0] = __ldg(reinterpret_cast<const uint32_t*>(row + j - 4));
-      mw[k][1] = __ldg(reinterpret_cast<const uint32_t*>(row + j));
-    } else {
-      mw[k][0] = mw[k][1] = 0u;
-      for (int m = 0; m < 8; ++m)
-        mw[k][m >> 2] |= (uint32_t)__ldg(row + wrap(j - 4 + m, Wh)) << (8 * (m & 3));
-    }
-  }
-  // PAN rows 2i-2 .. 2i+3: bytes of columns c-4 .. c+11
-  uint32_t w[6][4];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const uint8_t* row = u.pan_row(2 * i - 2 + k);
-    if (c >= 4 && c + 12 <= W) {
-      w[k][0] = __ldg(reinterpret_cast<const uint32_t*>(row + c - 4));
-      const uint2 m = __ldg(reinterpret_cast<const uint2*>(row + c));
-      w[k][1] = m.x;
-      w[k][2] = m.y;
-      w[k][3] = __ldg(reinterpret_cast<const uint32_t*>(row + c + 8));
-    } else {
-      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0u;
-      for (int m = 0; m < 16; ++m)
-        w[k][m >> 2] |= (uint32_t)__ldg(row + wrap(c - 4 + m, W)) << (8 * (m & 3));
-    }
-  }
   double v[2][5];  // vertical synthesis at output rows 2i, 2i+1, half-columns j-1 .. j+3
 #pragma unroll
   for (int J = 0; J < 5; ++J) {
@@ -612,7 +579,7 @@ __device__ __forceinline__ void fix_unit_u8(const U8Band& u, int i, int c) {
       // within 1e-5 of an integer (the float32 cast moves o by <= 2^-17 * 256
       // = 2e-6 here); those take the exact float32 route, and within 1e-9
       // (float64 orders differ by << 1e-9) the reference's own order
-      const double v = o + 0.5, fl = floor(v), fr = v - fl;
+      const double vh = o + 0.5, fl = floor(vh), fr = vh - fl;
       uint32_t q;
       if (fr > 1e-5 && fr < 1.0 - 1e-5) {
         q = (uint32_t)min(max((int)fl, 0), 255);
@@ -637,12 +604,37 @@ __device__ __forceinline__ void fix_unit_u8(const U8Band& u, int i, int c) {
   }
 }
 
-// The queued unit e = i << 11 | tt << 4 | b (row pair i, consumer thread tt,
-// band b) of the CTA whose column band starts at `base`
-template <int NB>
-__device__ __forceinline__ void fix_entry_u8(const FuseArgs<uint8_t>& a, uint32_t e, int base) {
-  fix_unit_u8(u8_band<NB>(a, (int)(e & 15u)), (int)(e >> 11), base + 8 * (int)((e >> 4) & 0x7fu));
+// The same recomputation with the unit's rows taken from the streaming
+// kernel's shared-memory ring: sA, sB, sC are the slots holding PAN rows
+// (2i-2, 2i-1), (2i, 2i+1), (2i+2, 2i+3) and MS rows i-2, i-1, i (slot layout
+// of produce_rows: [PAN row | PAN row | NB x MS row], each with a HALO-byte
+// left halo); rel = the unit's first column within the CTA's column band.
+template <int NB, int CW>
+__device__ __forceinline__ void fix_unit_ring(const U8Band& u, int i, int c, int rel, int b,
+                                              const uint8_t* sA, const uint8_t* sB,
+                                              const uint8_t* sC) {
+  constexpr int HALO = 16, PROW = CW + 2 * HALO, MROW = CW / 2 + HALO;
+  uint32_t w[6][4], mw[2][2];
+  const uint8_t* src[3] = {sA, sB, sC};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const uint32_t* p =
+        reinterpret_cast<const uint32_t*>(src[k >> 1] + (k & 1) * PROW + HALO + rel - 4);
+    w[k][0] = p[0];
+    w[k][1] = p[1];
+    w[k][2] = p[2];
+    w[k][3] = p[3];
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(
+        src[k + 1] + 2 * PROW + b * MROW + HALO + (rel >> 1) - 4);
+    mw[k][0] = p[0];
+    mw[k][1] = p[1];
+  }
+  fix_unit_core(u, i, c, w, mw);
 }
+
 
 template <int NB, int NCW, int MINB, int CVT, bool EXACT>
 __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
@@ -699,9 +691,17 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   // conflict-free), not in 5*NB registers: registers then fit 4 CTAs per SM
   float4* ep4 = reinterpret_cast<float4*>(empty + S) + t;  // [NB][NCW*32]
   float* ep1 = reinterpret_cast<float*>(reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + t;
-  // EXACT: this warp's list of units to recompute (global memory)
-  uint32_t* fixq = EXACT ? a.fixq + ((size_t)blockIdx.x * NCW + warp) * a.fixcap : nullptr;
+  // EXACT: per-warp queues of units to recompute (shared memory, after the
+  // carry arrays; two row pairs of every band fit, so they never overflow)
+  // and their lengths
+  constexpr int QW = 2 * 32 * NB;
+  uint32_t* qbase = reinterpret_cast<uint32_t*>(
+      reinterpret_cast<float*>(reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) +
+      NB * NCW * 32);
+  uint32_t* fixq = qbase + warp * QW;
+  int* qcnt = reinterpret_cast<int*>(qbase + NCW * QW);
   int fixn = 0;  // queued units (warp-uniform)
+  const unsigned lt_mask = (1u << lane) - 1u;
 
   // v2 unrolls the row-pair loop twice; v3 does not (its longer body spills
   // at 96 registers when unrolled: 0.80 vs 0.67 ms without the fix-up)
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
           if constexpr (EXACT) {
             // o + 0.5 + 2^-9 (the offset rides in pa) onto the 2^-8 grid,
             // rounded down: bytes 1-2 = 0x4000 + integer part, byte 0 =
-            // fraction (see the v3 comment above fix_unit_u8)
+            // fraction (see the v3 comment above quantize_ref)
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
               const int k = m >> 1;
@@ -798,9 +798,9 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
                                (near & 0xFF000000u) == 0u);
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, flag);
             if (bal) {  // warp-uniform
-              const int pos = fixn + __popc(bal & ((1u << lane) - 1u));
-              if (flag && pos < a.fixcap)
-                fixq[pos] = ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b;
+              if (flag)
+                fixq[fixn + __popc(bal & lt_mask)] =
+                    ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b;
               fixn += __popc(bal);
             }
           } else {
@@ -849,43 +849,48 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
 #pragma unroll
     for (int J = 0; J < 5; ++J) rprev[J] = rn[J];
     __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[s]);
-  }
-  if constexpr (EXACT) {
-    if (lane == 0) a.fixn[(size_t)blockIdx.x * NCW + warp] = fixn;
-  }
-}
-
-// The 8 bpp D4 fix-up: one warp per (task, consumer warp) list of
-// fuse_d4_u8x8_kernel<..., EXACT>, one queued unit per lane in turn (the
-// lists' entries and bytes were written by the previous kernel on the same
-// stream). An overflowing list (inputs with many values at rounding
-// boundaries) re-does every unit of that warp's column group and row run.
-template <int NB, int NCW>
-__global__ void __launch_bounds__(32 * NCW)
-    fix_u8_kernel(const FuseArgs<uint8_t> a) {
-  if (a.fix_mode == 3) return;  // timing experiment: detection only
-  constexpr int CW = 256 * NCW;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cb = (int)(blockIdx.x % (unsigned)a.n_colbands);
-  const int rt = (int)(blockIdx.x / (unsigned)a.n_colbands);
-  const int base = cb * CW;
-  const int len = min(CW, a.W - base);
-  const int npairs = a.rows >> 1;
-  const int i0 = rt * a.pairs_per_task;
-  const int i1 = min(i0 + a.pairs_per_task, npairs);
-  const int t = warp * 32 + lane;
-  const bool valid = 8 * t < len;
-  const size_t list = (size_t)blockIdx.x * NCW + warp;
-  const int fixn = a.fixn[list];
-  const uint32_t* fixq = a.fixq + list * a.fixcap;
-  const bool over = fixn > a.fixcap;
-  const int cnt = over ? (valid ? (i1 - i0) * NB : 0) : (fixn - lane + 31) / 32;
-  for (int k = 0; k < cnt; ++k) {
-    const uint32_t e = over ? ((uint32_t)(i0 + k / NB) << 11) | ((uint32_t)t << 4) |
-                                  (uint32_t)(k % NB)
-                            : fixq[lane + 32 * k];
-    fix_entry_u8<NB>(a, e, base);
+    if constexpr (!EXACT) {
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+    } else {
+      // Every second row pair (and after the last) the CTA's consumer threads
+      // recompute the units queued in the last two row pairs, one per thread
+      // in turn, from the rows still in the ring: a slot is released three
+      // row pairs late (loads n-3 .. n are resident here), so nothing is
+      // re-read from memory, and the four warps' queues are pooled so the
+      // lanes are well filled (~90 units per CTA per batch on random data;
+      // each warp working through its own queue measured 1.12 vs 1.02 ms).
+      if (n >= 2 && ((n & 1) || n == nloads - 1)) {
+        if (lane == 0) qcnt[warp] = fixn;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * NCW) : "memory");
+        if (a.fix_mode != 3) {
+          int cnt[NCW], total = 0;
+#pragma unroll
+          for (int q = 0; q < NCW; ++q) {
+            cnt[q] = qcnt[q];
+            total += cnt[q];
+          }
+          for (int k = t; k < total; k += 32 * NCW) {
+            int q = 0, idx = k;
+#pragma unroll
+            for (int qq = 0; qq < NCW - 1; ++qq)
+              if (q == qq && idx >= cnt[qq]) {
+                idx -= cnt[qq];
+                ++q;
+              }
+            const uint32_t e = qbase[q * QW + idx];
+            const int ei = (int)(e >> 11), tt = (int)((e >> 4) & 0x7fu), eb = (int)(e & 15u);
+            const int li = ei - i0 + 2;  // load holding PAN rows 2i+2, 2i+3
+            fix_unit_ring<NB, CW>(u8_band<NB>(a, eb), ei, base + 8 * tt, 8 * tt, eb,
+                                  slots + (size_t)((li - 2) % S) * SLOT,
+                                  slots + (size_t)((li - 1) % S) * SLOT,
+                                  slots + (size_t)(li % S) * SLOT);
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * NCW) : "memory");
+        fixn = 0;
+      }
+      if (lane == 0 && n >= 3) tma::mbar_arrive(&empty[(n - 3) % S]);
+    }
   }
 }
 
@@ -899,9 +904,11 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   int S = tune.d4_stages > 0 ? tune.d4_stages : (int)((32 * 1024) / SLOT);
   if (S < 2) S = 2;
   if (S > 16) S = 16;
-  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer thread)
+  // ring + barriers + the E(i-1) carry (20 bytes per band per consumer
+  // thread) + (EXACT) the per-warp fix-up queues and their lengths
   const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
-                      (size_t)NB * NCW * 32 * 20;
+                      (size_t)NB * NCW * 32 * 20 +
+                      (EXACT ? (size_t)NCW * (2 * 32 * NB + 1) * sizeof(uint32_t) : 0);
   a.fix_mode = EXACT ? tune.u8_fix_mode : 0;
   auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT, EXACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -914,57 +921,8 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   a.pairs_per_task = P;
   const long long n_row = (npairs + P - 1) / P;
   a.n_tasks = n_row * a.n_colbands;
-  if constexpr (!EXACT) {
-    kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
-    return cudaGetLastError();
-  } else {
-    // WF_U8_CHUNK_PAIRS (experiment): row chunks (whole-plane launches only:
-    // a chunk's halo rows are its neighbours' rows of the same plane), each
-    // streaming kernel followed by its fix-up kernel, so that the fix-up
-    // re-reads rows the chunk has just pulled through L2. Measured slower on
-    // the Landsat scene (one-wave chunks 1.58 ms, 2368-row chunks 1.36 ms,
-    // unchunked 1.06 ms; profiles/r02_u8_fixup_timing.log): the per-chunk
-    // ramps cost more than the re-reads.
-    long long chunk_pairs = tune.u8_chunk_pairs > 0 ? tune.u8_chunk_pairs : npairs;
-    const bool chunked = a.halo_pitch == a.pan_pitch && npairs > 2 * chunk_pairs;
-    if (!chunked) chunk_pairs = npairs;
-    const long long tasks_max = ((chunk_pairs + P - 1) / P) * a.n_colbands;
-    // the fix-up lists, stream-ordered (re-entrant: one allocation per call)
-    a.fixcap = u8_fix_cap(NB);
-    const size_t lists = (size_t)tasks_max * NCW;
-    void* scratch = nullptr;
-    if ((e = cudaMallocAsync(&scratch, lists * ((size_t)a.fixcap + 1) * sizeof(uint32_t), s)) !=
-        cudaSuccess)
-      return e;
-    a.fixn = static_cast<int*>(scratch);
-    a.fixq = reinterpret_cast<uint32_t*>(a.fixn + lists);
-    for (long long p0 = 0; p0 < npairs && e == cudaSuccess; p0 += chunk_pairs) {
-      const long long np = npairs - p0 < chunk_pairs ? npairs - p0 : chunk_pairs;
-      FuseArgs<uint8_t> c = a;
-      if (chunked) {
-        const long long r0 = 2 * p0, r1 = 2 * (p0 + np);
-        c.pan = a.pan + r0 * a.pan_pitch;
-        c.rows = (int)(r1 - r0);
-        c.pan_top = p0 == 0 ? a.pan_top : a.pan + (r0 - 2) * a.pan_pitch;
-        c.pan_bot = p0 + np == npairs ? a.pan_bot : a.pan + r1 * a.pan_pitch;
-        for (int b = 0; b < a.nbands; ++b) {
-          c.ms[b] = a.ms[b] + p0 * a.ms_pitch;
-          c.ms_top[b] = p0 == 0 ? a.ms_top[b] : a.ms[b] + (p0 - 1) * a.ms_pitch;
-          c.out[b] = a.out[b] + r0 * a.out_pitch;
-        }
-        c.n_tasks = ((np + P - 1) / P) * a.n_colbands;
-      }
-      kern<<<(unsigned)c.n_tasks, 32 * (NCW + 1), smem, s>>>(c, S);
-      e = cudaGetLastError();
-      if (e == cudaSuccess) {
-        fix_u8_kernel<NB, NCW><<<(unsigned)c.n_tasks, 32 * NCW, 0, s>>>(c);
-        e = cudaGetLastError();
-      }
-      if (e == cudaSuccess) count_extra_launches(p0 == 0 ? 1 : 2);
-    }
-    const cudaError_t f = cudaFreeAsync(scratch, s);
-    return e == cudaSuccess ? f : e;
-  }
+  kern<<<(unsigned)a.n_tasks, 32 * (NCW + 1), smem, s>>>(a, S);
+  return cudaGetLastError();
 }
 
 template <bool EXACT>
@@ -975,14 +933,14 @@ static cudaError_t launch_u8x8_v(const FuseArgs<uint8_t>& a, cudaStream_t s,
   // 3 CTAs/SM at 128 registers measured 0.509, 5 CTAs/SM at 72 registers
   // spill and measured 0.510)
   switch (a.nbands) {
-    case 1: return launch_u8x8_nb<1, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 2: return launch_u8x8_nb<2, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 3: return launch_u8x8_nb<3, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 4: return launch_u8x8_nb<4, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 5: return launch_u8x8_nb<5, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 6: return launch_u8x8_nb<6, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 7: return launch_u8x8_nb<7, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
-    case 8: return launch_u8x8_nb<8, 4, WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 1: return launch_u8x8_nb<1, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 2: return launch_u8x8_nb<2, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 3: return launch_u8x8_nb<3, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 4: return launch_u8x8_nb<4, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 5: return launch_u8x8_nb<5, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 6: return launch_u8x8_nb<6, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 7: return launch_u8x8_nb<7, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
+    case 8: return launch_u8x8_nb<8, 4, EXACT ? WF_U8X8E_MIN_CTAS : WF_U8X8_MIN_CTAS, 2, EXACT>(a, s, tune);
     default: return cudaErrorInvalidValue;
   }
 }

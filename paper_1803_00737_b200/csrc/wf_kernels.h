@@ -29,9 +29,6 @@ struct FuseArgs {
   int nbands;
   int wide;  // float64 with 32-byte aligned rows: 256-bit PAN loads / output stores
   int fix_mode;  // 8 bpp D4 v3: 0 normal, 1 every unit re-done in float64, 2 in reference order
-  uint32_t* fixq;  // 8 bpp D4 v3: per (task, consumer warp) list of units to recompute
-  int* fixn;       //   and its length (> capacity: overflow, re-do the warp's whole run)
-  int fixcap;      //   entries per list
   int rows;  // PAN rows in this launch (even)
   int W;     // PAN columns (even)
   // filled by the launcher
@@ -49,7 +46,6 @@ struct LaunchTuning {
   int haar_u8_ppt;      // >0: 8 bpp Haar row pairs per thread
   int d4_u8_variant;    // 8 bpp D4: 0 = v3 byte-exact (default), 1 = v1 (4 columns), 2 = v2
   int u8_fix_mode;      // v3 test hook: 1 = recompute every unit, 2 = ... in reference order
-  int u8_chunk_pairs;   // >0: row pairs per chunk of the byte-exact 8 bpp D4 launches
   int d4_ldg;           // 1: force the register-path D4 kernel (no bulk copies)
   int no_wide;          // 1: float64 rows through 128-bit accesses, not 256-bit
   int exact_rows;       // >0: coefficient rows per CTA of the one-pass exact D4 kernel
@@ -60,8 +56,7 @@ struct LaunchTuning {
 // The tuning knobs of the environment (WF_HAAR_PPT, WF_D4_*, ...), read once
 // per process (capi.cu); experiments set them before the first call.
 const LaunchTuning& env_tuning();
-// kernels a launcher issued beyond the one the C ABI counts per call
-void count_extra_launches(int n);
+
 
 // vec: 16-byte vector path legal; tma: the bulk-copy D4 pipeline is legal
 // (W % 8 == 0, every row 16-byte aligned).

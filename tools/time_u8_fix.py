@@ -1,7 +1,7 @@
-"""Split the 8 bpp D4 v3 kernel's time: full (detect + queue + float64
-fix-up), detection without the fix-up (WF_U8_FIX=skipfix), no detection
-(nodetect), and the round-1 v2 kernel; plus how many units the fix-up
-re-does (counted by diffing against the no-fix-up bytes)."""
+"""Split the byte-exact 8 bpp D4 kernel's time: full (detect + queue + the
+in-ring float64 fix-up), detection without the fix-up (WF_U8_FIX=skipfix), no
+detection (nodetect), and the round-1 v2 kernel; plus how many bytes the
+fix-up changes (counted by diffing against the no-fix-up bytes)."""
 import os
 import sys
 
@@ -20,13 +20,9 @@ del sc
 lib = _native.load()
 mp = _native.ptr_array([m.data_ptr() for m in ms])
 res = {}
-chunks = sys.argv[1:] or ["0"]  # WF_U8_CHUNK_PAIRS values for the full v3 pair (0 = auto)
-cases = [("v3", "", ch) for ch in chunks] + [("v3", "skipfix", "0"), ("v3", "nodetect", "0"),
-                                            ("v2", "", "0")]
-for variant, fix, ch in cases:
+for variant, fix in (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", "")):
     os.environ["WF_D4_U8"] = variant
     os.environ["WF_U8_FIX"] = fix
-    os.environ["WF_U8_CHUNK_PAIRS"] = ch
     _native.reload_tuning()
     out = [torch.empty((H, W), dtype=torch.uint8, device="cuda") for _ in ms]
     op = _native.ptr_array([o.data_ptr() for o in out])
@@ -41,8 +37,7 @@ for variant, fix, ch in cases:
         run()
     e1.record()
     torch.cuda.synchronize()
-    print(f"{variant} {fix or 'full'} chunk_pairs={ch}: {e0.elapsed_time(e1) / 10:.3f} ms",
-          flush=True)
+    print(f"{variant} {fix or 'full'}: {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
     res[(variant, fix)] = out
 full, skip = res[("v3", "")], res[("v3", "skipfix")]
 changed = sum(int((a != b).sum()) for a, b in zip(full, skip))
