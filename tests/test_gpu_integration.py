@@ -113,3 +113,63 @@ def test_reference_suite_against_drop_in(ref):
         out[-3000:]
     routed = re.search(r"B200 drop-in calls routed: (.*)", out)
     assert routed and "fuse_dwt=" in routed.group(1) and "worker_tiles=" in routed.group(1)
+
+
+@pytest.mark.gpu
+def test_transfer_8bpp_float64_pan_matches_reference(ref):
+    """fuse_tiled(transfer_8bpp=True) quantises a float64 PAN (and
+    float64 resampled bands) in float64, like the reference's wire_planes;
+    values just below a .5 boundary must round the reference's way."""
+    import wavefuse.fusion as F
+    import wavefuse.tiling as T
+    import wavefuse.wavelet as Wv
+
+    import paper_1803_00737_b200 as wf
+
+    rng = np.random.default_rng(8)
+    # many values within float32 rounding of k + 0.5
+    base = rng.integers(0, 255, (128, 256)).astype(np.float64) + 0.5
+    pan = base - rng.choice([0.0, 1e-9, 2e-8], base.shape)
+    ms = [rng.uniform(0, 255, (32, 64)) for _ in range(2)]  # not half size: resampled (float64)
+    for kind, rkind in ((wf.WaveletKind.HAAR, Wv.WaveletKind.HAAR),
+                        (wf.WaveletKind.DAUB4, Wv.WaveletKind.DAUB4)):
+        got = wf.fuse_tiled(pan, ms, wf.DwtReplace(kind), wf.plan_grid(256, 128, 2, 2),
+                            transfer_8bpp=True)
+        want = T.fuse_tiled(pan, ms, F.DwtReplace(rkind), T.plan_grid(256, 128, 2, 2),
+                            transfer_8bpp=True)
+        for g, w_ in zip(got, want):
+            assert g.dtype == np.uint8 and np.array_equal(g, w_)
+
+
+@pytest.mark.gpu
+def test_exact_mixed_dtypes_match_reference(ref):
+    """exact mode with a float32 PAN and float64 bands keeps the
+    bands' float64 values in LL (fusion.py:149) and casts once at the end --
+    bit-identical to the reference, device and host paths, fuse_dwt / fuse /
+    fuse_tiled."""
+    import wavefuse.fusion as F
+    import wavefuse.tiling as T
+    import wavefuse.wavelet as Wv
+    import torch
+
+    import paper_1803_00737_b200 as wf
+
+    rng = np.random.default_rng(9)
+    pan = rng.uniform(0, 255, (96, 160)).astype(np.float32)
+    ms = [rng.uniform(0, 255, (48, 80)) for _ in range(3)]  # float64
+    for kind, rkind in ((wf.WaveletKind.HAAR, Wv.WaveletKind.HAAR),
+                        (wf.WaveletKind.DAUB4, Wv.WaveletKind.DAUB4)):
+        want = F.fuse(pan, ms, F.DwtReplace(rkind))
+        assert want[0].dtype == np.float32
+        got = wf.fuse(pan, ms, wf.DwtReplace(kind), exact=True)
+        dev = wf.fuse(torch.from_numpy(pan).cuda(), [torch.from_numpy(m).cuda() for m in ms],
+                      wf.DwtReplace(kind), exact=True)
+        one = wf.fuse_dwt(pan, ms[0], kind, exact=True)
+        for g, d, w_ in zip(got, dev, want):
+            assert g.dtype == np.float32 and np.array_equal(g, w_)
+            assert d.dtype == torch.float32 and np.array_equal(d.cpu().numpy(), w_)
+        assert np.array_equal(one, F.fuse_dwt(pan, ms[0], rkind))
+        gt = wf.fuse_tiled(pan, ms, wf.DwtReplace(kind), wf.plan_grid(160, 96, 2, 2), exact=True)
+        wt = T.fuse_tiled(pan, ms, F.DwtReplace(rkind), T.plan_grid(160, 96, 2, 2))
+        for g, w_ in zip(gt, wt):
+            assert np.array_equal(g, w_)
