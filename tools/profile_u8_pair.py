@@ -11,6 +11,10 @@ from paper_1803_00737_b200 import _native
 from paper_1803_00737_b200.fusion import _quantize_dev
 from paper_1803_00737_b200.scene import DeviceScene
 
+if os.environ.get("WF_LIB"):  # A/B: profile another build of the library
+    import pathlib
+    _native.LIB_PATH = pathlib.Path(os.environ["WF_LIB"]).resolve()
+
 H, W, B = 14000, 16000, 6
 sc = DeviceScene.synthetic(H, W, B)
 pan = _quantize_dev(sc.pan)

@@ -12,6 +12,11 @@ import paper_1803_00737_b200 as wf
 from paper_1803_00737_b200 import _device, _native
 from paper_1803_00737_b200.scene import DeviceScene
 
+if os.environ.get("WF_LIB"):  # A/B: time another build of the library
+    import pathlib
+    _native.LIB_PATH = pathlib.Path(os.environ["WF_LIB"]).resolve()
+    print(f"library: {_native.LIB_PATH.name}")
+
 h = int(sys.argv[1]) if len(sys.argv) > 1 else 14000
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 16000
 B = 6

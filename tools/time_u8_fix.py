@@ -9,6 +9,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 from paper_1803_00737_b200 import _native
+
+if len(sys.argv) > 1:  # A/B: time another build of the library
+    import pathlib
+    _native.LIB_PATH = pathlib.Path(sys.argv[1]).resolve()
+    print(f"library: {sys.argv[1]}")
 from paper_1803_00737_b200.fusion import _quantize_dev
 from paper_1803_00737_b200.scene import DeviceScene
 
@@ -20,7 +25,10 @@ del sc
 lib = _native.load()
 mp = _native.ptr_array([m.data_ptr() for m in ms])
 res = {}
-for variant, fix in (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", "")):
+modes = (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", ""))
+if os.environ.get("WF_TIME_MODES"):  # e.g. "v3:skipfix,v2:"
+    modes = tuple(tuple(m.split(":")) for m in os.environ["WF_TIME_MODES"].split(","))
+for variant, fix in modes:
     os.environ["WF_D4_U8"] = variant
     os.environ["WF_U8_FIX"] = fix
     _native.reload_tuning()
@@ -39,6 +47,8 @@ for variant, fix in (("v3", ""), ("v3", "skipfix"), ("v3", "nodetect"), ("v2", "
     torch.cuda.synchronize()
     print(f"{variant} {fix or 'full'}: {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
     res[(variant, fix)] = out
+if ("v3", "") not in res or ("v3", "skipfix") not in res or ("v2", "") not in res:
+    sys.exit(0)
 full, skip = res[("v3", "")], res[("v3", "skipfix")]
 changed = sum(int((a != b).sum()) for a, b in zip(full, skip))
 v2diff = sum(int((a != b).sum()) for a, b in zip(full, res[("v2", "")]))
