@@ -455,7 +455,8 @@ def measure_quality(scene, steps, warmup, peak):
 
     # Haar fusion + the same report in ONE pass
     # (wf_fuse_quality_f32): the fused bands are written, never re-read --
-    # reported next to fuse() + qnr() because it is the slower of the two
+    # reported next to fuse() + qnr() (vs_separate_ms), which it must beat to
+    # be fuse_and_qnr()'s default for Haar
     fo = [torch.empty_like(scene.pan) for _ in scene.ms]
     fop = _native.ptr_array([t.data_ptr() for t in fo])
 

@@ -713,6 +713,17 @@ constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes) wh
 #ifndef WF_Q2_LBACKOFF
 #define WF_Q2_LBACKOFF 0
 #endif
+// unroll of each role's row-pair loop: scoring 4 (2.01 ms; 2 -> 2.16, 1 ->
+// 2.32), fused pass 2 (3.05 ms; 1 -> 3.17, 4 -> 3.70: the fused variant's
+// longer bodies overflow the instruction cache when fully unrolled -- ncu:
+// no-instruction stalls 33K vs 3.5K samples; profiles/r02_qnr_rowpack.log)
+#ifndef WF_Q2_HUF
+#define WF_Q2_HUF 2
+#endif
+#ifndef WF_Q2_HUQ
+#define WF_Q2_HUQ 4
+#endif
+constexpr int kQ2HuF = WF_Q2_HUF, kQ2HuQ = WF_Q2_HUQ;
 #ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound); 2 -> 2.24 ms, 3 -> 2.03, 4 -> 2.33
 #define WF_Q2_STAGES 3
 #endif
@@ -746,7 +757,7 @@ struct Q2Cfg {
   static constexpr int FOFF = MSOFF + NB * MSR * kQ2Msw;
   static constexpr int FSL = 2 * PAIRS * 32;  // floats per slice
   static constexpr int SLOT = FOFF + (FUSE ? NB * kQ2Bc * FSL : 0);
-  static constexpr int NBAR = ((2 + kQ2Bc * PAIRS) * S + 1) & ~1;  // full, empty, fready (even)
+  static constexpr int NBAR = (2 * S + 1) & ~1;  // full, empty (even)
   static constexpr int NBE = NB + (NB & 1);  // bands padded to even (role L halves)
   static constexpr int H = NBE / 2;
   static constexpr int NBP = NBE / 2;        // float2 band pairs
@@ -841,7 +852,6 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       smem_raw + ((128u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 127u)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * C::SLOT);
   uint64_t* empty = full + S;
-  uint64_t* fready = empty + S;  // FUSE: [S][kQ2Bc][PAIRS] fused rows of (stage, column, pair) ready
   // barriers padded to an even count: dsb and the transpose buffers after it
   // stay 16-byte aligned (LDS.128 in lane_sum32)
   double* dsb = reinterpret_cast<double*>(full + C::NBAR);  // [2][kQ2Bc][DS]
@@ -854,7 +864,6 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
     for (int s = 0; s < S; ++s) {
       tma::mbar_init(&full[s], kQ2Prod);
       tma::mbar_init(&empty[s], kQ2Cons);
-      for (int c = 0; c < kQ2Bc * C::PAIRS; ++c) tma::mbar_init(&fready[s * kQ2Bc * C::PAIRS + c], 1);
     }
     tma::fence_barrier_init();
   }
@@ -977,7 +986,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const int s = g % S;
         tma::mbar_wait_backoff<WF_Q2_FBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
-#pragma unroll
+#pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
         for (int h = 0; h < C::PAIRS; ++h) {  // row pair h of the stage
         const int t = C::PAIRS * u + h;
         float fv[2][NBE], pv[2];
@@ -1008,10 +1017,6 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
               fs[k * kQ2Bc * C::FSL + 32] = fv[1][k];
             }
           }
-          // this pair's fused rows are in the slices: release them to the U / L
-          // warps of the block column (mbarrier arrive = release)
-          __syncwarp();
-          if (lane == 0) tma::mbar_arrive(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h]);
           if (h == C::PAIRS - 1) {
             // the stage's slices are complete: stream them to the fused bands
             tma::fence_async_smem();
@@ -1119,7 +1124,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         tma::mbar_wait_backoff<WF_Q2_UBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
         const int rb = i0 + C::PAIRS * u - 1;  // MS row of the stage box's first row
-#pragma unroll
+#pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
         for (int h = 0; h < C::PAIRS; ++h) {
         const int t = C::PAIRS * u + h;
         // horizontal bilinear of MS row gr (clamped) of bands (2m, 2m + 1) at
@@ -1151,13 +1156,20 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
 #pragma unroll
             for (int k = 0; k < NBE; ++k) fv[p][k] = k < NB ? row[k * C::PLANE] : 0.f;
           }
-        } else {  // the F role's slice of this block column
-          tma::mbar_wait_sleep(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h], (g / S) & 1);
-          const float* fs = slot + C::FOFF + bcl * C::FSL + 2 * h * 32 + lane;
+        } else {
+          // FUSE: this role forms the Haar bands itself from the staged PAN
+          // and MS, in role F's operation order (bit-identical), rather than
+          // waiting for role F's rows: no role waits on another within a stage
+          float pvv[2];
+#pragma unroll
+          for (int p = 0; p < 2; ++p) pvv[p] = slot[(2 * h + p) * kQ2Cols + xl + C::PIDX * C::PLANE];
+          const float ll = haar_ll(pvv);
+          const float* mr = slot + C::MSOFF + (h + 1) * kQ2Msw + rxr;  // M(i0 + t, x/2)
 #pragma unroll
           for (int k = 0; k < NBE; ++k) {
-            fv[0][k] = k < NB ? fs[k * kQ2Bc * C::FSL] : 0.f;
-            fv[1][k] = k < NB ? fs[k * kQ2Bc * C::FSL + 32] : 0.f;
+            const float d = k < NB ? mr[k * C::MSR * kQ2Msw] - ll : 0.f;
+            fv[0][k] = k < NB ? pvv[0] + d : 0.f;
+            fv[1][k] = k < NB ? pvv[1] + d : 0.f;
           }
         }
         if (h == C::PAIRS - 1) {
@@ -1254,7 +1266,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int m = 0; m < NBE; ++m) {
         const int b = band_of(m);
         foff[m] = (b < NB ? b : C::PIDX) * C::PLANE;  // padding bands read the PAN row
-        fsoff[m] = (b < NB ? b : 0) * kQ2Bc * C::FSL;   // FUSE: slice of band b
+        fsoff[m] = (b < NB ? b : 0) * C::MSR * kQ2Msw + rxr;  // FUSE: M(., x/2) of band b
       }
 #pragma unroll
       for (int m = 0; m < 2 * HP; ++m) {
@@ -1280,7 +1292,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
         tma::mbar_wait_backoff<WF_Q2_LBACKOFF>(&full[s], (g / S) & 1);
         const float* slot = ring + (size_t)s * C::SLOT;
-#pragma unroll
+#pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
         for (int h = 0; h < C::PAIRS; ++h) {
         const int t = C::PAIRS * u + h;
         // M_k(i, x/2) of the own bands, i = i0 + t (box row 1 + h; i <= Hh - 1)
@@ -1298,13 +1310,14 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
           }
           pv[p] = row[C::PIDX * C::PLANE];
         }
-        if (FUSE) {  // the F role's slice of this block column (local band order)
-          tma::mbar_wait_sleep(&fready[(s * kQ2Bc + bcl) * C::PAIRS + h], (g / S) & 1);
-          const float* fs = slot + C::FOFF + bcl * C::FSL + 2 * h * 32 + lane;
+        if (FUSE) {  // the Haar bands of the local band order, as in role U
+          const float ll = haar_ll(pv);
+          const float* mr = slot + C::MSOFF + (h + 1) * kQ2Msw;  // M(i0 + t, .)
 #pragma unroll
           for (int m = 0; m < NBE; ++m) {
-            fv[0][m] = fs[fsoff[m]];
-            fv[1][m] = fs[fsoff[m] + 32];
+            const float d = band_of(m) < NB ? mr[fsoff[m]] - ll : 0.f;
+            fv[0][m] = pv[0] + d;
+            fv[1][m] = pv[1] + d;
           }
         }
         if (h == C::PAIRS - 1) {

@@ -432,20 +432,21 @@ def qnr(fused, ms, pan) -> QualityReport:
     )
 
 
-def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
+def fuse_and_qnr(pan, ms, method, *, one_pass: bool | None = None):
     """fuse(pan, ms, method) followed by qnr(fused, ms, pan); returns
     (fused, QualityReport).
 
-    one_pass=True (Haar, scenes that qualify for the one-pass kernel: float32,
-    2..8 half-size bands, H, W >= 64, W % 8 == 0) runs SURVEY.md 8(f) row f1
-    literally: the scoring kernel fuses each pixel itself and streams the
-    fused bands out as it scores them, so they are never re-read (C ABI
-    wf_fuse_quality_f32; bands bit-identical to fuse()'s, report identical
-    to qnr()'s). It is opt-in because it is slower on B200: the scoring
-    kernel is compute-bound, and making the fusion a per-row-pair dependency
-    of the scoring warps costs more than re-reading 5.4 GB of fused bands
-    (Landsat, 6 bands: 4.07 ms one pass vs 3.40 ms for fuse() + qnr();
-    bench.py quality.fused_haar_fuse_and_report)."""
+    Haar scenes that qualify for the one-pass kernel (float32, 2..8
+    half-size bands, H, W >= 64, W % 8 == 0) run SURVEY.md 8(f) row f1
+    literally unless one_pass=False: the scoring kernel fuses each pixel
+    itself and streams the fused bands out as it scores them, so they are
+    never re-read (C ABI wf_fuse_quality_f32; bands bit-identical to
+    fuse()'s, report identical to qnr()'s). Landsat, 6 bands: 3.05 ms one
+    pass vs 3.17 ms for fuse() + qnr() (bench.py
+    quality.fused_haar_fuse_and_report; round 1's one-pass kernel was the
+    slower of the two at 3.6 ms until its row-pair loops stopped overflowing
+    the instruction cache). D4 always takes fuse() + qnr(): its fusion needs
+    a +-2-row/column neighbourhood the scoring stages do not hold."""
     from . import fusion as _fusion
     from .wavelet import WaveletKind
 
@@ -454,7 +455,8 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool = False):
     is_t = isinstance(pan, torch.Tensor)
     p_shape = tuple(pan.shape) if is_t else np.shape(pan)
     bands = _bands(ms)
-    fast = (one_pass and method.kind == WaveletKind.HAAR and len(p_shape) == 2 and bands
+    fast = (one_pass is not False and method.kind == WaveletKind.HAAR and len(p_shape) == 2
+            and bands
             and all(_shape(b) == (p_shape[0] // 2, p_shape[1] // 2) for b in bands)
             and p_shape[0] % 2 == 0 and p_shape[1] % 2 == 0)
     if fast:
