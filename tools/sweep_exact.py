@@ -9,6 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 from paper_1803_00737_b200 import _native
+
+if os.environ.get("WF_LIB"):  # A/B: time another build of the library
+    import pathlib
+    _native.LIB_PATH = pathlib.Path(os.environ["WF_LIB"]).resolve()
 from paper_1803_00737_b200.scene import DeviceScene
 
 H, W, B = 14000, 16000, 6
