@@ -84,6 +84,13 @@ int64_t wf_launch_count(void);
 /* Re-read the WF_* tuning environment variables (read once at load time
    otherwise; experiment knobs only, results do not depend on them). */
 int wf_tuning_reload(void);
+/* Debug builds: 1 if this library was built with the device-side ring and
+   bounds invariants (python -m paper_1803_00737_b200._build --checked,
+   loaded with WF_CHECKED=1), else 0. wf_check_selftest() runs one failing
+   invariant: a checked build traps (and the CUDA context is lost -- call it
+   from a throwaway process); a product build returns WF_OK. */
+int wf_checked_build(void);
+int wf_check_selftest(void);
 
 /* ---- fused hot path (device buffers) ---------------------------------- */
 int wf_fuse_dwt_f32(int kind, const float* pan, int64_t pan_pitch, const float* ms,

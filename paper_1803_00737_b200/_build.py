@@ -45,25 +45,36 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
-def stale() -> bool:
-    if not LIB.exists():
+# the checked variant (device-side ring/bounds invariants, wf_common.cuh
+# WF_CHECK): a separate library and object directory, loaded only with
+# WF_CHECKED=1
+LIB_CHECKED = PKG / "libwavefuse_b200_checked.so"
+OBJ_CHECKED = PKG / "build_checked"
+
+
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    built = LIB.stat().st_mtime
+    built = lib.stat().st_mtime
     deps = sources() + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [HEADER]
     return any(p.stat().st_mtime > built for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
     """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
-    then link the shared library; the log of every step goes to build.log."""
-    if not force and not stale():
-        return LIB
-    OBJ.mkdir(exist_ok=True)
+    then link the shared library; the log of every step goes to build.log.
+    checked=True builds the WF_CHECKS variant (LIB_CHECKED)."""
+    lib = LIB_CHECKED if checked else LIB
+    objdir = OBJ_CHECKED if checked else OBJ
+    if not force and not stale(lib):
+        return lib
+    objdir.mkdir(exist_ok=True)
     inc = ["-I", str(ROOT / "include")]
+    extra = ["-DWF_CHECKS"] if checked else []
 
     def compile_one(src: Path):
-        obj = OBJ / (src.stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, *inc, "-c", "-o", str(obj), str(src)]
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *extra, *inc, "-c", "-o", str(obj), str(src)]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, proc
 
@@ -76,15 +87,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         log_text.append(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
         if proc.returncode != 0:
             failed.append((src, proc.stderr))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     if not failed:
         # peer.cu resolves cuMemGetAddressRange from libcuda at run time (-ldl)
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *[str(o) for _, o, _, _ in results], "-ldl"]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         log_text.append(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
         if proc.returncode != 0:
-            failed.append((LIB, proc.stderr))
-    log = PKG / "build.log"
+            failed.append((lib, proc.stderr))
+    log = PKG / ("build_checked.log" if checked else "build.log")
     log.write_text("\n".join(log_text))
     if failed:
         for _, err in failed:
@@ -92,10 +103,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write("\n".join(log_text))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                checked="--checked" in sys.argv))

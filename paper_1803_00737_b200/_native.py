@@ -8,6 +8,7 @@ from PyTorch (plumbing only); all compute happens in libwavefuse_b200.so.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 import threading
 from pathlib import Path
@@ -16,6 +17,9 @@ from . import errors
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libwavefuse_b200.so"
+if os.environ.get("WF_CHECKED", "") not in ("", "0"):
+    # the device-side-invariant build (_build.py --checked), for test runs
+    LIB_PATH = _PKG / "libwavefuse_b200_checked.so"
 HEADER_PATH = _PKG.parent / "include" / "wavefuse_b200.h"
 
 HAAR, DAUB4 = 1, 2
@@ -92,6 +96,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.wf_last_error.restype = ctypes.c_char_p
     lib.wf_launch_count.restype = c_i64
     lib.wf_tuning_reload.restype = c_int
+    lib.wf_checked_build.restype = c_int
+    lib.wf_check_selftest.restype = c_int
     lib.wf_ctx_create.argtypes = [c_int, c_int]
     lib.wf_ctx_create.restype = c_vp
     lib.wf_ctx_upload.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp]

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/wavefuse_b200.h"
+#include "wf_common.cuh"
 #include "wf_kernels.h"
 
 namespace wf {
@@ -559,11 +560,21 @@ int fuse_host_impl(wf_ctx* ctx, int kind, const T* pan, const T* const* ms, T* c
   return WF_OK;
 }
 
+// wf_check_selftest: one WF_CHECK that fails at run time (x is 0); in a
+// checked build it traps, which proves the invariants are compiled in
+__global__ void check_selftest_kernel(int x) { WF_CHECK(x == 1); }
+
 }  // namespace
 
 extern "C" {
 
 const char* wf_version(void) { return "wavefuse-b200 0.2.0 (sm_100a)"; }
+int wf_checked_build(void) { return wf::kCheckTagBytesPerSlot > 0 ? 1 : 0; }
+int wf_check_selftest(void) {
+  check_selftest_kernel<<<1, 1>>>(0);
+  cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? WF_OK : cuda_status(e, "check selftest");
+}
 int wf_tuning_reload(void) {
   wf::g_tuning = wf::read_tuning();
   return WF_OK;

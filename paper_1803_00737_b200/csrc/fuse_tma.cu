@@ -136,7 +136,7 @@ __device__ __forceinline__ void store4_out(T* p, const Acc (&o)[4], bool wide = 
 template <typename T, int NB, int CW, int HALO, bool KEEP = false>
 __device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slots, uint64_t* full,
                                              uint64_t* empty, int base, int len, int i0,
-                                             int nloads, int lane) {
+                                             int nloads, int lane, uint32_t* tags = nullptr) {
   // KEEP: the copies mark their lines evict_last in L2 (the 8 bpp fix-up
   // re-reads the task's rows after the stream has moved on)
   const uint64_t pol = KEEP ? tma::policy_evict_last() : 0ull;
@@ -163,6 +163,9 @@ __device__ __forceinline__ void produce_rows(const FuseArgs<T>& a, int S, T* slo
     if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
     __syncwarp();
     const bool with_ms = n >= 1;
+#ifdef WF_CHECKS
+    if (lane == 0 && tags) tags[s] = (uint32_t)n;  // published by the arrive below
+#endif
     if (lane == 0)
       tma::mbar_arrive_expect_tx(&full[s],
                                  2 * pan_row_bytes + (with_ms ? NB * ms_row_bytes : 0u));
@@ -215,6 +218,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
   T* slots = reinterpret_cast<T*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)S * SLOT * sizeof(T) + 15) & ~size_t(15)));
   uint64_t* empty = full + S;
+  uint32_t* tags = reinterpret_cast<uint32_t*>(empty + S);  // checked builds: [S]
+  (void)tags;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = (int)(blockIdx.x % (unsigned)a.n_colbands);
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
   __syncthreads();
 
   if (warp == NCW) {
-    produce_rows<T, NB, CW, HALO>(a, S, slots, full, empty, base, len, i0, nloads, lane);
+    produce_rows<T, NB, CW, HALO>(a, S, slots, full, empty, base, len, i0, nloads, lane, tags);
     return;
   }
 
@@ -256,6 +261,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
   for (int n = 0; n < nloads; ++n) {
     const int s = n % S;
     tma::mbar_wait_sleep(&full[s], (n / S) & 1);
+    WF_CHECK(tags[s] == (uint32_t)n);
     const T* slot = slots + (size_t)s * SLOT;
     Acc v[2][8];  // PAN cols c-2 .. c+5 of the slot's two rows
 #pragma unroll
@@ -361,6 +367,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), TmaTraits<T>::MIN_CTAS)
     for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int jj = 0; jj < 3; ++jj) rprev[q][jj] = rn[q][jj];
+    WF_CHECK(tags[s] == (uint32_t)n);  // still this load's bytes
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&empty[s]);
   }
@@ -669,8 +676,12 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   __syncthreads();
 
   if (warp == NCW) {
+    constexpr int QWP = 2 * 32 * NB;
+    uint32_t* ptags = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(
+                          reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + NB * NCW * 32) +
+                      NCW * QWP + NCW;
     produce_rows<uint8_t, NB, CW, HALO, EXACT>(a, S, slots, full, empty, base, len, i0, nloads,
-                                               lane);
+                                               lane, ptags);
     return;
   }
 
@@ -701,6 +712,12 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   uint32_t* fixq = qbase + warp * QW;
   int* qcnt = reinterpret_cast<int*>(qbase + NCW * QW);
   int fixn = 0;  // queued units (warp-uniform)
+  // checked builds: [S] load index per ring slot, after the queue lengths
+  uint32_t* tags = reinterpret_cast<uint32_t*>(
+      reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(
+          reinterpret_cast<float4*>(empty + S) + NB * NCW * 32) + NB * NCW * 32) +
+      NCW * QW + NCW);
+  (void)tags;
   const unsigned lt_mask = (1u << lane) - 1u;
 
   // v2 unrolls the row-pair loop twice; v3 does not (its longer body spills
@@ -709,6 +726,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
   for (int n = 0; n < nloads; ++n) {
     const int s = n % S;
     tma::mbar_wait_sleep(&full[s], (n / S) & 1);
+    WF_CHECK(tags[s] == (uint32_t)n);
     const uint8_t* slot = slots + (size_t)s * SLOT;
     // PAN columns c-2 .. c+9 of the slot's two rows, packed (row 0, row 1)
     float2 x[12];
@@ -802,6 +820,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
                 fixq[fixn + __popc(bal & lt_mask)] =
                     ((uint32_t)i << 11) | ((uint32_t)t << 4) | (uint32_t)b;
               fixn += __popc(bal);
+              WF_CHECK(fixn <= QW);
             }
           } else {
 #pragma unroll
@@ -880,6 +899,10 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
             const uint32_t e = qbase[q * QW + idx];
             const int ei = (int)(e >> 11), tt = (int)((e >> 4) & 0x7fu), eb = (int)(e & 15u);
             const int li = ei - i0 + 2;  // load holding PAN rows 2i+2, 2i+3
+            // the three slots still hold loads li-2 .. li (released 3 late)
+            WF_CHECK(li >= 2 && li <= n && n - li <= 1);
+            WF_CHECK(tags[(li - 2) % S] == (uint32_t)(li - 2) &&
+                     tags[(li - 1) % S] == (uint32_t)(li - 1) && tags[li % S] == (uint32_t)li);
             fix_unit_ring<NB, CW>(u8_band<NB>(a, eb), ei, base + 8 * tt, 8 * tt, eb,
                                   slots + (size_t)((li - 2) % S) * SLOT,
                                   slots + (size_t)((li - 1) % S) * SLOT,
@@ -889,6 +912,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), MINB)
         asm volatile("bar.sync 1, %0;" ::"n"(32 * NCW) : "memory");
         fixn = 0;
       }
+      WF_CHECK(n < 3 || tags[(n - 3) % S] == (uint32_t)(n - 3));
       if (lane == 0 && n >= 3) tma::mbar_arrive(&empty[(n - 3) % S]);
     }
   }
@@ -908,7 +932,10 @@ static cudaError_t launch_u8x8_nb(const FuseArgs<uint8_t>& a0, cudaStream_t s,
   // thread) + (EXACT) the per-warp fix-up queues and their lengths
   const size_t smem = (((size_t)S * SLOT + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t) +
                       (size_t)NB * NCW * 32 * 20 +
-                      (EXACT ? (size_t)NCW * (2 * 32 * NB + 1) * sizeof(uint32_t) : 0);
+                      (EXACT || kCheckTagBytesPerSlot
+                           ? (size_t)NCW * (2 * 32 * NB + 1) * sizeof(uint32_t)
+                           : 0) +
+                      (size_t)S * kCheckTagBytesPerSlot;
   a.fix_mode = EXACT ? tune.u8_fix_mode : 0;
   auto kern = fuse_d4_u8x8_kernel<NB, NCW, MINB, CVT, EXACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -968,8 +995,8 @@ static cudaError_t launch_tma_nb(const FuseArgs<T>& a0, cudaStream_t s, const La
     if (S < 2) S = 2;
     if (S > 8) S = 8;
   }
-  const size_t smem =
-      (((size_t)S * SLOT * sizeof(T) + 15) & ~size_t(15)) + 2 * S * sizeof(uint64_t);
+  const size_t smem = (((size_t)S * SLOT * sizeof(T) + 15) & ~size_t(15)) +
+                      2 * S * sizeof(uint64_t) + (size_t)S * kCheckTagBytesPerSlot;
   auto kern = fuse_d4_tma_kernel<T, NB, NCW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

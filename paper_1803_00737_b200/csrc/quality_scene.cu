@@ -856,6 +856,10 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
   // stay 16-byte aligned (LDS.128 in lane_sum32)
   double* dsb = reinterpret_cast<double*>(full + C::NBAR);  // [2][kQ2Bc][DS]
   float* trs = reinterpret_cast<float*>(dsb + 2 * kQ2Bc * C::DS);  // [kQ2Cons][kQ2TrRows][kTrPad]
+  // checked builds: [S] stage index per ring slot (wf_common.cuh)
+  uint32_t* tags =
+      reinterpret_cast<uint32_t*>(trs + (WF_Q2_SHFL ? 0 : kQ2Cons * kQ2TrRows * kTrPad));
+  (void)tags;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.nbr * a.ncx;
@@ -882,6 +886,9 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const int s = g % S, r = g / S;
         if (r > 0 && lane == 0) tma::mbar_wait_sleep(&empty[s], (r - 1) & 1);
         __syncwarp();
+#ifdef WF_CHECKS
+        if (lane == 0) tags[s] = (uint32_t)g;  // published by the arrive below
+#endif
         if (lane == 0) tma::mbar_arrive_expect_tx(&full[s], kStageBytes);
         __syncwarp();
         float* slot = ring + (size_t)s * C::SLOT;
@@ -985,6 +992,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
         tma::mbar_wait_backoff<WF_Q2_FBACKOFF>(&full[s], (g / S) & 1);
+        WF_CHECK(tags[s] == (uint32_t)g);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
         for (int h = 0; h < C::PAIRS; ++h) {  // row pair h of the stage
@@ -1035,6 +1043,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
+          WF_CHECK(tags[s] == (uint32_t)g);  // still this stage's bytes
           if (lane == 0) tma::mbar_arrive(&empty[s]);
           ++g;
         }
@@ -1122,6 +1131,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
         tma::mbar_wait_backoff<WF_Q2_UBACKOFF>(&full[s], (g / S) & 1);
+        WF_CHECK(tags[s] == (uint32_t)g);
         const float* slot = ring + (size_t)s * C::SLOT;
         const int rb = i0 + C::PAIRS * u - 1;  // MS row of the stage box's first row
 #pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
@@ -1174,6 +1184,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
+          WF_CHECK(tags[s] == (uint32_t)g);  // still this stage's bytes
           if (lane == 0) tma::mbar_arrive(&empty[s]);
           ++g;
         }
@@ -1291,6 +1302,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         const int s = g % S;
         if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
         tma::mbar_wait_backoff<WF_Q2_LBACKOFF>(&full[s], (g / S) & 1);
+        WF_CHECK(tags[s] == (uint32_t)g);
         const float* slot = ring + (size_t)s * C::SLOT;
 #pragma unroll(FUSE ? kQ2HuF : kQ2HuQ)
         for (int h = 0; h < C::PAIRS; ++h) {
@@ -1322,6 +1334,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         }
         if (h == C::PAIRS - 1) {
           __syncwarp();
+          WF_CHECK(tags[s] == (uint32_t)g);  // still this stage's bytes
           if (lane == 0) tma::mbar_arrive(&empty[s]);
           ++g;
         }
@@ -2480,7 +2493,8 @@ static size_t q2_smem() {
   using C = Q2Cfg<NB, FUSE>;
   return 128 + (size_t)C::S * C::SLOT * sizeof(float) + C::NBAR * sizeof(uint64_t) +
          (size_t)2 * kQ2Bc * C::DS * sizeof(double) +
-         (WF_Q2_SHFL ? 0 : (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float)) + 16;
+         (WF_Q2_SHFL ? 0 : (size_t)kQ2Cons * kQ2TrRows * kTrPad * sizeof(float)) +
+         (size_t)C::S * kCheckTagBytesPerSlot + 16;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no

@@ -11,7 +11,35 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
+// Checked builds (python -m paper_1803_00737_b200._build --checked, loaded
+// with WF_CHECKED=1): device-side invariants of the bulk-copy rings -- every
+// ring slot carries the index of the load it holds, written by the producer
+// before the copies are issued and verified by each consumer after its full
+// wait and again before it releases the slot (a slot overwritten early, read
+// late or released twice traps) -- plus queue and index bounds. Compiled out
+// of the product library. (compute-sanitizer is not available on the GPU
+// pool; this is the substitute for its racecheck/synccheck on these rings.)
+#ifdef WF_CHECKS
+#define WF_CHECK(cond)                                                                  \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("WF_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,     \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                              \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#define WF_CHECK_TAG_BYTES 4
+#else
+#define WF_CHECK(cond) ((void)0)
+#define WF_CHECK_TAG_BYTES 0
+#endif
+
 namespace wf {
+
+// smem bytes per ring slot for the checked build's load tags (0 otherwise)
+constexpr int kCheckTagBytesPerSlot = WF_CHECK_TAG_BYTES;
 
 // Wire codes of the wavelet kinds (cluster.py:81-83 uses 1 = Haar, 2 = D4).
 enum Kind : int { kHaar = 1, kDaub4 = 2 };

@@ -34,6 +34,17 @@ def test_version_string(lib):
     assert b"sm_100a" in lib.wf_version()
 
 
+def test_product_library_is_not_the_checked_build(lib):
+    """The device-side invariants (WF_CHECKS) are compiled into the separate
+    debug library only; the default load is the product build."""
+    import os
+
+    if os.environ.get("WF_CHECKED", "") not in ("", "0"):
+        pytest.skip("WF_CHECKED set: the checked build is loaded on purpose")
+    assert _native.LIB_PATH.name == "libwavefuse_b200.so"
+    assert lib.wf_checked_build() == 0
+
+
 FAKE = 0x1000  # never dereferenced: validation returns first
 
 
