@@ -475,6 +475,38 @@ def measure_quality(scene, steps, warmup, peak):
     torch.cuda.synchronize()
     per_fused = e0.elapsed_time(e1) / n
     same = all(torch.equal(a_, b_) for a_, b_ in zip(fo, scene.out))
+    # D4 through the same call: the fusion kernel, then the report kernel on
+    # its output (the fastest schedule measured; the SM-partitioned overlap,
+    # WF_FQ_OVERLAP=1, measured slower -- profiles/r02_fq_overlap.log)
+    scene.launcher(WaveletKind.DAUB4)()
+    torch.cuda.synchronize()
+
+    def run_fused_d4():
+        _native.check(lib.wf_fuse_quality_f32(2, scene.pan.data_ptr(), w, mp, w // 2, fop, w, nb,
+                                              h, w, ws.data_ptr(), out.data_ptr(),
+                                              flag.data_ptr(), _device.stream_ptr()))
+
+    for _ in range(warmup):
+        run_fused_d4()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(n):
+        run_fused_d4()
+    e1.record()
+    torch.cuda.synchronize()
+    per_fused_d4 = e0.elapsed_time(e1) / n
+    same_d4 = all(torch.equal(a_, b_) for a_, b_ in zip(fo, scene.out))
+    for _ in range(warmup):
+        run()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(n):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    per_d4_report = e0.elapsed_time(e1) / n
+    scene.launcher(WaveletKind.HAAR)()
+    torch.cuda.synchronize()
     return {
         "ms_per_report": round(per, 4),
         "report": {"ergas": rep.ergas, "qnr": rep.qnr, "d_lambda": rep.d_lambda, "d_s": rep.d_s},
@@ -489,7 +521,33 @@ def measure_quality(scene, steps, warmup, peak):
             "fused_bands_identical_to_fuse": same,
             "api": "wf_fuse_quality_f32 / paper_1803_00737_b200.fuse_and_qnr(one_pass=True)",
         },
+        "fused_d4_fuse_and_report": {
+            "ms_per_scene": round(per_fused_d4, 4),
+            "vs_separate_ms": round(per_d4_report + d4_fuse_ms(scene), 4),
+            "fused_bands_identical_to_fuse": same_d4,
+            "schedule": "D4 fusion kernel, then the report kernel, in one call (an SM-partitioned "
+                        "overlap of the two measured slower: profiles/r02_fq_overlap.log)",
+            "api": "wf_fuse_quality_f32(kind=2) / paper_1803_00737_b200.fuse_and_qnr",
+        },
     }
+
+
+def d4_fuse_ms(scene, reps=10):
+    """CUDA-event time of one whole-scene D4 fusion launch."""
+    import torch
+
+    from paper_1803_00737_b200 import WaveletKind
+
+    run = scene.launcher(WaveletKind.DAUB4)
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def hmean_fuse_ms(scene, reps=10):

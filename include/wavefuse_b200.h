@@ -314,12 +314,16 @@ int wf_quality_scene_f32(const float* const* fused, const float* const* ms, cons
 int wf_quality_scene_f64(const double* const* fused, const double* const* ms, const double* pan,
                          int64_t f_pitch, int64_t ms_pitch, int64_t pan_pitch, int nbands, int h,
                          int w, void* workspace, double* out, int* undecidable, void* stream);
-/* SURVEY.md 8(f) row f1, second half: Haar fusion and its quality report in
- * ONE pass over the scene -- fusion.py:153-183 fuse(pan, ms, DwtReplace(HAAR))
- * followed by metrics.py:178-199 qnr(fused, ms, pan), without re-reading the
- * fused bands. Writes out[0..nbands) (bit-identical to wf_fuse_bands_f32) and
- * the report in wf_quality_scene_f32's layout; same shape/alignment rules and
- * workspace (wf_quality_scene_workspace_bytes). kind must be WF_HAAR. */
+/* SURVEY.md 8(f) row f1, second half: fusion and its quality report in ONE
+ * call -- fusion.py:153-183 fuse(pan, ms, DwtReplace(kind)) followed by
+ * metrics.py:178-199 qnr(fused, ms, pan). Haar: one pass over the scene (the
+ * scoring kernel fuses each pixel itself and streams the bands out; they are
+ * never re-read). D4: the fusion kernel, then the scoring kernel on its
+ * output (the fastest schedule measured; WF_FQ_OVERLAP=1 selects an
+ * SM-partitioned overlap of the two, slower). Writes out[0..nbands)
+ * (bit-identical to wf_fuse_bands_f32) and the report in
+ * wf_quality_scene_f32's layout (bit-identical to it on those bands); same
+ * shape/alignment rules and workspace (wf_quality_scene_workspace_bytes). */
 int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
                         int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
                         int w, void* workspace, double* report, int* undecidable, void* stream);

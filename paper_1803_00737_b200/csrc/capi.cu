@@ -53,6 +53,10 @@ static LaunchTuning read_tuning() {
   v.exact_transforms = getenv("WF_EXACT_TRANSFORMS") != nullptr;
   const char* q = getenv("WF_QNR_KERNEL");
   v.qnr_kernel = (q && q[0] == 'v' && q[1] == '1') ? 1 : (q && q[0] == 'v' && q[1] == '3') ? 3 : 2;
+  v.fq_ctas = num("WF_FQ_CTAS");
+  v.fq_band_rows = num("WF_FQ_BAND_ROWS");
+  v.fq_overlap = num("WF_FQ_OVERLAP");
+  v.fq_debug = num("WF_FQ_DEBUG");
   return v;
 }
 static LaunchTuning g_tuning = read_tuning();
@@ -1075,7 +1079,7 @@ int wf_quality_scene_f64(const double* const* fused, const double* const* ms, co
 int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const float* const* ms,
                         int64_t ms_pitch, float* const* out, int64_t out_pitch, int nbands, int h,
                         int w, void* workspace, double* report, int* undecidable, void* stream) {
-  if (kind != WF_HAAR) return fail(WF_ERR_VALUE, "fused fusion + quality pass is Haar only");
+  if (int e = check_kind(kind)) return e;
   if (!out || !ms || !pan || !workspace || !report || !undecidable)
     return fail(WF_ERR_VALUE, "null pointer argument");
   if (nbands < 2 || nbands > wf::kMaxBandsPerLaunch)
@@ -1092,10 +1096,32 @@ int wf_fuse_quality_f32(int kind, const float* pan, int64_t pan_pitch, const flo
     if (!out[b] || !ms[b]) return fail(WF_ERR_VALUE, "null band pointer %d", b);
     if (!al16(out[b]) || !al16(ms[b])) return fail(WF_ERR_VALUE, "band %d not 16-byte aligned", b);
   }
-  cudaError_t e = wf::launch_fuse_quality_haar(nbands, pan, ms, out, out_pitch, ms_pitch,
-                                               pan_pitch, h, w, workspace, report, undecidable,
-                                               (cudaStream_t)stream);
-  if (e == cudaSuccess) g_launches += 6;
+  // Haar: one pass (the report kernel forms the bands itself, 3.05 vs 3.20
+  // ms for the two kernels); D4: the fusion kernel, then the report kernel on
+  // its output (3.20 ms). WF_FQ_OVERLAP=1: the SM-partitioned overlap of the
+  // two (either kind; measured 3.4-10 ms, profiles/r02_fq_overlap.log).
+  const wf::LaunchTuning& tune = wf::env_tuning();
+  cudaError_t e = cudaSuccess;
+  if (tune.fq_overlap) {
+    int launches = 0;
+    e = wf::launch_fuse_quality_overlap(kind == WF_HAAR ? wf::kHaar : wf::kDaub4, nbands, pan,
+                                        ms, out, out_pitch, ms_pitch, pan_pitch, h, w, workspace,
+                                        report, undecidable, (cudaStream_t)stream, &launches);
+    g_launches += launches;
+  } else if (kind == WF_HAAR) {
+    e = wf::launch_fuse_quality_haar(nbands, pan, ms, out, out_pitch, ms_pitch, pan_pitch, h, w,
+                                     workspace, report, undecidable, (cudaStream_t)stream);
+    if (e == cudaSuccess) g_launches += 6;
+  } else {
+    const float* const* cout = out;
+    if (int rc = fuse_common<float>(kind, pan, pan_pitch, nullptr, nullptr, 0, ms, nullptr,
+                                    ms_pitch, out, out_pitch, nbands, h, w, false,
+                                    (cudaStream_t)stream))
+      return rc;
+    e = wf::launch_quality_scene(nbands, cout, ms, pan, out_pitch, ms_pitch, pan_pitch, h, w,
+                                 workspace, report, undecidable, (cudaStream_t)stream);
+    if (e == cudaSuccess) g_launches += 4;
+  }
   return cuda_status(e, "wf_fuse_quality_f32");
 }
 

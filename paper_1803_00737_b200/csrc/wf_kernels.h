@@ -51,6 +51,11 @@ struct LaunchTuning {
   int exact_rows;       // >0: coefficient rows per CTA of the one-pass exact D4 kernel
   int exact_transforms; // 1: exact mode as forward + inverse transform kernels
   int qnr_kernel;       // QNR scene kernel: 2 = v2 role-split (default), 1 = v1, 3 = v3 (tile)
+  int fq_ctas;          // >0: report CTAs of the overlapped fuse + report (default SMs - 28)
+  int fq_band_rows;     // >0: row band of the overlapped fuse + report (rounded to 32)
+  int fq_overlap;       // 1: fuse + report as the SM-partitioned overlap (measured slower; default:
+                        //    Haar one pass, D4 the fusion kernel then the report kernel)
+  int fq_debug;         // overlapped path experiments: 1 = no report kernel, 2 = report after fusion
 };
 
 // The tuning knobs of the environment (WF_HAAR_PPT, WF_D4_*, ...), read once
@@ -138,6 +143,14 @@ cudaError_t launch_fuse_quality_haar(int nb, const float* P, const float* const*
                                      float* const* O, long long op, long long mp, long long pp,
                                      int h, int w, void* workspace, double* out,
                                      int* undecidable, cudaStream_t s);
+// Fusion (Haar or D4) and its quality report overlapped: the fusion runs in
+// row bands on an internal stream while the persistent report kernel scores
+// each band as soon as it is written (the bands come back from L2).
+cudaError_t launch_fuse_quality_overlap(int kind, int nb, const float* P, const float* const* M,
+                                        float* const* O, long long op, long long mp,
+                                        long long pp, int h, int w, void* workspace,
+                                        double* out, int* undecidable, cudaStream_t s,
+                                        int* launches);
 cudaError_t launch_quality_scene64(int nb, const double* const* F, const double* const* M,
                                    const double* P, long long fp, long long mp, long long pp,
                                    int h, int w, void* workspace, double* out, int* undecidable,

@@ -432,16 +432,17 @@ def qnr(fused, ms, pan) -> QualityReport:
     )
 
 
-def _fuse_quality_launch(p_t, m_t, outs):
-    """Queue the one-pass Haar fusion + report (wf_fuse_quality_f32) of device
-    float32 planes into `outs` (contiguous h x w float32) on the current
-    stream; returns the report vector and the undecidable flag (not read)."""
+def _fuse_quality_launch(p_t, m_t, outs, code=1):
+    """Queue the fusion + report call (wf_fuse_quality_f32; code 1 = Haar, one
+    pass; 2 = D4, fusion then report) of device float32 planes into `outs`
+    (contiguous h x w float32) on the current stream; returns the report
+    vector and the undecidable flag (not read)."""
     lib = _native.load()
     n = len(m_t)
     h, w = p_t.shape
     ws, out, flag = _scene_buffers(n, h, w, p_t.device)
     _native.check(lib.wf_fuse_quality_f32(
-        1, p_t.data_ptr(), p_t.stride(0), _native.ptr_array([t.data_ptr() for t in m_t]),
+        code, p_t.data_ptr(), p_t.stride(0), _native.ptr_array([t.data_ptr() for t in m_t]),
         m_t[0].stride(0), _native.ptr_array([o.data_ptr() for o in outs]), w, n, h, w,
         ws.data_ptr(), out.data_ptr(), flag.data_ptr(), _device.stream_ptr()))
     return out, flag
@@ -449,17 +450,20 @@ def _fuse_quality_launch(p_t, m_t, outs):
 
 def fuse_and_qnr_async(pan, ms, method, *, out=None):
     """fuse_and_qnr() for device tensors without the read-back: returns
-    (fused, PendingReport). Haar scenes that qualify take the one-pass kernel
-    (written into `out` if given: contiguous float32 h x w tensors on the
-    PAN's device, one per band); anything else runs fuse() (into new tensors)
-    and qnr_async(). bench.py's batch workload (C5) scores its scenes so."""
+    (fused, PendingReport). Float32 Haar and D4 scenes that qualify take
+    wf_fuse_quality_f32 (Haar: the one-pass kernel; D4: fusion then report in
+    one call), written into `out` if given (contiguous float32 h x w tensors
+    on the PAN's device, one per band); anything else runs fuse() (into new
+    tensors) and qnr_async(). bench.py's batch workload (C5) scores its
+    scenes so."""
     from . import fusion as _fusion
     from .wavelet import WaveletKind
 
     if not isinstance(method, _fusion.DwtReplace):
         raise TypeError(f"unknown fusion method {method!r}")
     bands = _bands(ms)
-    if method.kind == WaveletKind.HAAR and isinstance(pan, torch.Tensor) and pan.is_cuda \
+    if method.kind in (WaveletKind.HAAR, WaveletKind.DAUB4) and isinstance(pan, torch.Tensor) \
+            and pan.is_cuda \
             and pan.dtype == torch.float32 and pan.dim() == 2 and bands \
             and all(isinstance(b, torch.Tensor) and b.dtype == torch.float32 for b in bands):
         h, w = pan.shape
@@ -477,7 +481,8 @@ def fuse_and_qnr_async(pan, ms, method, *, out=None):
                                       for o in out):
                 raise ValueError("out: one contiguous float32 (h, w) tensor per band on the "
                                  "PAN's device")
-            vec, flag = _fuse_quality_launch(p_t, m_t, out)
+            code = 1 if method.kind == WaveletKind.HAAR else 2
+            vec, flag = _fuse_quality_launch(p_t, m_t, out, code)
             return out, PendingReport((out, m_t, p_t), (None, vec, flag), n, 2)
     fused = _fusion.fuse(pan, ms, method)
     return fused, qnr_async(fused, ms, pan)
@@ -496,8 +501,11 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool | None = None):
     pass vs 3.17 ms for fuse() + qnr() (bench.py
     quality.fused_haar_fuse_and_report; round 1's one-pass kernel was the
     slower of the two at 3.6 ms until its row-pair loops stopped overflowing
-    the instruction cache). D4 always takes fuse() + qnr(): its fusion needs
-    a +-2-row/column neighbourhood the scoring stages do not hold."""
+    the instruction cache). D4 scenes that qualify take the same call, which
+    runs the D4 fusion kernel and then the scoring kernel on its output (3.20
+    ms, the fastest schedule measured: an SM-partitioned overlap of the two,
+    WF_FQ_OVERLAP=1, measured 3.4 ms at best -- both kernels need every SM,
+    profiles/r02_fq_overlap.log); one_pass=False forces fuse() + qnr()."""
     from . import fusion as _fusion
     from .wavelet import WaveletKind
 
@@ -506,7 +514,8 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool | None = None):
     is_t = isinstance(pan, torch.Tensor)
     p_shape = tuple(pan.shape) if is_t else np.shape(pan)
     bands = _bands(ms)
-    fast = (one_pass is not False and method.kind == WaveletKind.HAAR and len(p_shape) == 2
+    fast = (one_pass is not False and method.kind in (WaveletKind.HAAR, WaveletKind.DAUB4)
+            and len(p_shape) == 2
             and bands
             and all(_shape(b) == (p_shape[0] // 2, p_shape[1] // 2) for b in bands)
             and p_shape[0] % 2 == 0 and p_shape[1] % 2 == 0)
@@ -520,7 +529,8 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool | None = None):
         if p_t is not None and p_t.dtype == torch.float32 and \
                 _scene_ok((*m_t, p_t), n, h, w, 2) and all(t.dtype == torch.float32 for t in m_t):
             outs = [torch.empty((h, w), dtype=torch.float32, device=p_t.device) for _ in m_t]
-            out, flag = _fuse_quality_launch(p_t, m_t, outs)
+            out, flag = _fuse_quality_launch(p_t, m_t, outs,
+                                             1 if method.kind == WaveletKind.HAAR else 2)
             rep = (qnr(outs, m_t, p_t) if int(flag.item())
                    else _scene_report(out.cpu().numpy(), n, 2))
             return (outs if is_t else [_device.to_host(o) for o in outs]), rep
