@@ -719,6 +719,11 @@ constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes) wh
 #ifndef WF_QNR_F64CELL  // ERGAS 2x2 sums in float64 (1) or FP32 TwoSums (0)
 #define WF_QNR_F64CELL 1
 #endif
+// role L loads its lane pair's two columns by LDS.64 and forms its own cells
+// without partner shuffles (1), or one column per lane plus shuffles (0)
+#ifndef WF_Q2_LPAIR
+#define WF_Q2_LPAIR 1
+#endif
 // back-off (ns) between full-barrier probes of the F / U / L role warps (0:
 // the plain suspend-hint wait); the F role runs ahead of the other two.
 // F 200 ns: 2.035 -> 2.015 ms; F 800 ns: 2.014 (slower on small scenes);
@@ -1349,6 +1354,63 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
         float2 raw[HP];
 #pragma unroll
         for (int j = 0; j < HP; ++j) raw[j] = make_float2(msr[moff[2 * j]], msr[moff[2 * j + 1]]);
+#if WF_Q2_LPAIR
+        // The lane pair's two columns (xc = xl & ~1, xc + 1) of the own bands
+        // and of the PAN, one LDS.64 each: every lane forms its own bands'
+        // 2x2 cells and the PAN cell from its own loads -- no partner-column
+        // shuffles, half the shared-memory loads. The sums are those of the
+        // shuffle form below bit for bit: float64 additions of float32 pairs
+        // and the TwoSum error terms do not depend on the operand order.
+        float2 fo[2][H], pq[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const float* row = slot + (2 * h + p) * kQ2Cols + (xl & ~1);
+          if (!FUSE) {
+#pragma unroll
+            for (int m = 0; m < H; ++m) fo[p][m] = *reinterpret_cast<const float2*>(row + foff[m]);
+          }
+          pq[p] = *reinterpret_cast<const float2*>(row + C::PIDX * C::PLANE);
+        }
+        if (FUSE) {  // the Haar bands of the own bands, as in role U
+          const float ll = ((pq[0].x + pq[0].y) + (pq[1].x + pq[1].y)) * 0.25f;
+          const float* mr = slot + C::MSOFF + (h + 1) * kQ2Msw;  // M(i0 + t, .)
+#pragma unroll
+          for (int m = 0; m < H; ++m) {
+            const float d = band_of(m) < NB ? mr[fsoff[m]] - ll : 0.f;
+            fo[0][m] = make_float2(pq[0].x + d, pq[0].y + d);
+            fo[1][m] = make_float2(pq[1].x + d, pq[1].y + d);
+          }
+        }
+        if (h == C::PAIRS - 1) {
+          __syncwarp();
+          WF_CHECK(tags[s] == (uint32_t)g);  // still this stage's bytes
+          if (lane == 0) tma::mbar_arrive(&empty[s]);
+          ++g;
+        }
+        // PAN cell: the exact (hi, lo) of the 4-pixel sum (both lanes agree)
+        float2 sp2, tp2;
+        two_sum2(pq[0], pq[1], sp2, tp2);
+        float S_, T_;
+        two_sum(sp2.x, sp2.y, S_, T_);
+        const float plo = T_ + (tp2.x + tp2.y);
+        const float dpd = 0.25f * ((S_ - kph) + (plo - kpl));
+        lwp += dpd;
+        lwpp = fmaf(dpd, dpd, lwpp);
+        // the own bands' exact 2x2 sums in float64, e = S/4 - m one rounding
+        // (metrics.py:31-42,117)
+        float ef[2 * HP];
+#pragma unroll
+        for (int m = 0; m < 2 * HP; ++m) {
+          if (m < H) {
+            const double S = ((double)fo[0][m].x + (double)fo[1][m].x) +
+                             ((double)fo[0][m].y + (double)fo[1][m].y);
+            const float mv = (m & 1) ? raw[m >> 1].y : raw[m >> 1].x;
+            ef[m] = (float)fma(S, 0.25, -(double)mv);
+          } else {
+            ef[m] = 0.f;
+          }
+        }
+#else
         float fv[2][NBE], pv[2];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
@@ -1404,6 +1466,9 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
             ef[m] = 0.f;
           }
         }
+#endif  // WF_QNR_F64CELL
+#endif  // WF_Q2_LPAIR
+#if WF_QNR_F64CELL || WF_Q2_LPAIR
         const float2 dpd2 = make_float2(dpd, dpd);
 #pragma unroll
         for (int j = 0; j < HP; ++j) {
