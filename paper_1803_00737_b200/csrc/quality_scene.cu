@@ -748,6 +748,9 @@ constexpr int kQ2TrRows = 24;           // transpose chunk (rows of 32 lanes) wh
 #define WF_Q2_HUQ 4
 #endif
 constexpr int kQ2HuF = WF_Q2_HUF, kQ2HuQ = WF_Q2_HUQ;
+#ifndef WF_Q2_PAIRS  // row pairs per ring stage: 4 (1.98 ms); 2 -> 2.04-2.19, 1 -> 3.18 (profiles/r02_qnr_stage_geometry.log)
+#define WF_Q2_PAIRS 4
+#endif
 #ifndef WF_Q2_STAGES  // ring depth in stages of 8 rows (NB >= 7: 2, smem-bound); 2 -> 2.24 ms, 3 -> 2.03, 4 -> 2.33
 #define WF_Q2_STAGES 3
 #endif
@@ -769,7 +772,7 @@ struct Q2Cfg {
   // ([NB][6][kQ2Msw]; rows outside the image arrive zero-filled and are
   // never read: the consumers clamp the row index first). One tensor copy
   // per plane and per band: 13 copies per 8 rows at B = 6.
-  static constexpr int PAIRS = 4;
+  static constexpr int PAIRS = WF_Q2_PAIRS;
   static constexpr int MSR = PAIRS + 2;
   static constexpr int PLANE = 2 * PAIRS * kQ2Cols;
   // FUSE (Haar fusion in the same pass): only the PAN is staged -- plane 0
@@ -1342,7 +1345,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
       const float2 q25 = make_float2(0.25f, 0.25f);
       for (int u = 0; u < 16 / C::PAIRS; ++u) {
         const int s = g % S;
-        if (u == 2) load_shifts(tile + gridDim.x, km_next, praw_next);
+        if (u == 8 / C::PAIRS) load_shifts(tile + gridDim.x, km_next, praw_next);  // mid-tile
         tma::mbar_wait_backoff<WF_Q2_LBACKOFF>(&full[s], (g / S) & 1);
         WF_CHECK(tags[s] == (uint32_t)g);
         const float* slot = ring + (size_t)s * C::SLOT;
