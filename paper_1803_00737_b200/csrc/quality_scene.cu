@@ -2962,8 +2962,23 @@ static cudaError_t launch_fq_overlap_nb(int kind, const float* P, const float* c
 
   // the fusion, band by band; halo rows from the scene itself (periodic wrap)
   const int Hh = h / 2;
+  // An error once the report kernel is running must not leave it waiting for
+  // bands that will never be signalled: publish "all bands" (the report is
+  // then garbage, the call returns the error) and join the streams.
+  bool report_live = false;
+  auto bail = [&](cudaError_t err) -> cudaError_t {
+    if (report_live) {
+      cudaMemsetAsync(ready, 0x7f, sizeof(int), r->aux);
+      cudaEventRecord(r->done, r->aux);
+      cudaStreamWaitEvent(s, r->done, 0);
+    }
+    return err;
+  };
   for (int b = 0; b < nbands_rows; ++b) {
-    if (b == 1 && tune.fq_debug == 0 && (e = launch_report()) != cudaSuccess) return e;
+    if (b == 1 && tune.fq_debug == 0) {
+      if ((e = launch_report()) != cudaSuccess) return bail(e);
+      report_live = ncta > 0;
+    }
     const int r0 = b * br, r1 = min(h, r0 + br);
     FuseArgs<float> f{};
     f.pan = P + (long long)r0 * pp;
@@ -2984,9 +2999,9 @@ static cudaError_t launch_fq_overlap_nb(int kind, const float* P, const float* c
     // the wrapper checked 16-byte rows and W % 8 == 0: vector and TMA paths legal
     if ((e = launch_fuse<float, float>(kind, f, true, kind == kDaub4, r->aux, tune)) !=
         cudaSuccess)
-      return e;
+      return bail(e);
     band_signal_kernel<<<1, 1, 0, r->aux>>>(ready, b + 1);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(e);
     *launches += 2;
   }
   if (nbands_rows == 1 && tune.fq_debug == 0 && (e = launch_report()) != cudaSuccess) return e;
