@@ -802,6 +802,26 @@ struct Q2Cfg {
   static constexpr int ND = NB / 2;     // odd-k diagonals
 };
 
+// acc + (x, x) * v lane-wise: one packed FFMA2 (fmaheavy sub-pipe only) or,
+// SCALAR, two FFMAs the fmalite sub-pipe can also take -- the same roundings
+#ifndef WF_Q2_SCALAR_FF
+#define WF_Q2_SCALAR_FF 0
+#endif
+#ifndef WF_Q2_SCALAR_UU
+#define WF_Q2_SCALAR_UU 0
+#endif
+template <int SCALAR>
+__device__ __forceinline__ float2 q2_ffma_pair(float x, float2 v, float2 acc) {
+  if constexpr (SCALAR) {
+    float rx, ry;
+    asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(rx) : "f"(x), "f"(v.x), "f"(acc.x));
+    asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(ry) : "f"(x), "f"(v.y), "f"(acc.y));
+    return make_float2(rx, ry);
+  } else {
+    return __ffma2_rn(make_float2(x, x), v, acc);
+  }
+}
+
 // lane-sum `n` (<= 32) rows of per-lane floats into ds[0..n) (float64)
 __device__ __forceinline__ void q2_flush(float* tr, int n, double* ds, int lane) {
   __syncwarp();
@@ -1118,8 +1138,8 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
             if (k & 1) fd[k >> 1] = fmaf(dk, dk, fd[k >> 1]);
 #pragma unroll
             for (int q = 0; q < C::npairs(k); ++q)
-              ff[C::base(k) + q] =
-                  __ffma2_rn(make_float2(dk, dk), d[(C::start(k) >> 1) + q], ff[C::base(k) + q]);
+              ff[C::base(k) + q] = q2_ffma_pair<WF_Q2_SCALAR_FF>(dk, d[(C::start(k) >> 1) + q],
+                                                                  ff[C::base(k) + q]);
           }
         }
         }
@@ -1267,8 +1287,8 @@ __global__ void __launch_bounds__(kQ2Threads, 1)
             if (k & 1) ud[k >> 1] = fmaf(dk, dk, ud[k >> 1]);
 #pragma unroll
             for (int q = 0; q < C::npairs(k); ++q)
-              uu[C::base(k) + q] =
-                  __ffma2_rn(make_float2(dk, dk), du[(C::start(k) >> 1) + q], uu[C::base(k) + q]);
+              uu[C::base(k) + q] = q2_ffma_pair<WF_Q2_SCALAR_UU>(dk, du[(C::start(k) >> 1) + q],
+                                                                  uu[C::base(k) + q]);
           }
         }
 #pragma unroll
