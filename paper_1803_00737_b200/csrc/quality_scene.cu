@@ -708,9 +708,12 @@ __global__ void band_signal_kernel(int* ready, int v) {
 // scores the block's Q pairs from the shared float64 sums. Results are the
 // same quantities in the same float32/float64 arithmetic as above.
 // ---------------------------------------------------------------------------
-constexpr int kQ2Bc = 5;                 // block columns per CTA
+#ifndef WF_Q2_BC
+#define WF_Q2_BC 5
+#endif
+constexpr int kQ2Bc = WF_Q2_BC;          // block columns per CTA
 constexpr int kQ2Cols = 32 * kQ2Bc;      // 160 PAN columns per tile
-constexpr int kQ2Msw = 96;               // staged MS segment: 80 cols + halo, one 384-B box
+constexpr int kQ2Msw = (16 * kQ2Bc + 8 + 15) / 16 * 16;  // staged MS segment: 80 cols + halo, one 384-B box
 constexpr int kQ2Cons = 3 * kQ2Bc;       // consumer warps
 constexpr int kQ2Prod = 1;               // producer warps
 constexpr int kQ2Threads = 32 * (kQ2Cons + kQ2Prod);
