@@ -1162,7 +1162,7 @@ def measure_batch(args, dist, rank, world, local_rank, steps, warmup):
         "scaling": "strong",
         "workload": (f"C5: {args.scenes} Landsat-shaped scenes x (Haar, D4), each fused and "
                      "scored (QNR/ERGAS) on the GPU (BASELINE configs[4]); Haar in one pass "
-                     "(fuse_and_qnr_async), D4 as fuse + qnr_async"),
+                     "(fuse_and_qnr_async), D4 as fusion then report in the same call"),
         "global_batch": args.scenes,
         "parallelism": f"scene-sharded x{world} (round-robin, no collective)",
         "scenes_per_rank": len(mine),
