@@ -60,3 +60,35 @@ def test_u8_random_shapes(kname):
             d = np.abs(g.astype(np.int32) - r.astype(np.int32))
             assert d.max() <= (0 if kname == "haar" else 1), (h, w, nb)
             assert np.array_equal(e, r), (h, w, nb)
+
+
+@pytest.mark.parametrize("kname", list(KINDS))
+def test_fuse_and_qnr_random_shapes(kname):
+    """fuse_and_qnr on random shapes and band counts (the one-call fuse +
+    report where the scene qualifies, fuse() + qnr() where it does not:
+    W % 8 != 0, H or W < 64, one band): fused bands as fuse() (float32 within
+    the north star's 1e-3 of the oracle) and the report within 1e-6 of the
+    pinned oracle's qnr() of those bands, device and numpy inputs."""
+    from oracle import cpu_quality as Q
+
+    rng = np.random.default_rng(500 + len(kname))
+    shapes = [(64, 64, 2), (96, 136, 3), (128, 200, 6), (160, 264, 8), (66, 130, 4),
+              (256, 96, 5), (34, 70, 2)]
+    m = wf.DwtReplace(KINDS[kname])
+    for h, w, nb in shapes:
+        pan = rng.uniform(0, 255, (h, w)).astype(np.float32)
+        bands = [rng.uniform(1, 255, (h // 2, w // 2)).astype(np.float32) for _ in range(nb)]
+        f_dev, rep_dev = wf.fuse_and_qnr(torch.from_numpy(pan).cuda(),
+                                         [torch.from_numpy(b).cuda() for b in bands], m)
+        f_np, rep_np = wf.fuse_and_qnr(pan, bands, m)
+        fused = [f.cpu().numpy() for f in f_dev]
+        for a, b, r in zip(fused, f_np, O.fuse(pan, bands, kname)):
+            assert np.array_equal(a, b), (h, w, nb)
+            assert np.max(np.abs(a.astype(np.float64) - r)) <= 1e-3, (h, w, nb)
+        ref = Q.qnr(fused, bands, pan)
+        for rep in (rep_dev, rep_np):
+            assert abs(rep.ergas - ref["ergas"]) <= 1e-6, (h, w, nb)
+            assert abs(rep.qnr - ref["qnr"]) <= 1e-6, (h, w, nb)
+            assert abs(rep.d_lambda - ref["d_lambda"]) <= 1e-6, (h, w, nb)
+            assert abs(rep.d_s - ref["d_s"]) <= 1e-6, (h, w, nb)
+            assert np.allclose(rep.q_per_band, ref["q_per_band"], rtol=0, atol=1e-6), (h, w, nb)
