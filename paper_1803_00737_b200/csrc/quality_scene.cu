@@ -2145,11 +2145,14 @@ struct QsArgs64 {
   int nbr, nbc, nbr_l, nbc_l;
 };
 
+// float64 report ring depth and block rows per warp run: 3 x 6 (3.63 ms);
+// was 5 x 8 (3.72); 2 x 8: 3.67, 3 x 12: 3.68, 7 x 8: 5.20; 3 CTAs/SM spills
+// (10.5 ms) -- profiles/r02_qnr64_sweep.log
 #ifndef WF_Q64_STAGES
-#define WF_Q64_STAGES 5
+#define WF_Q64_STAGES 3
 #endif
 #ifndef WF_Q64_RUN
-#define WF_Q64_RUN 8
+#define WF_Q64_RUN 6
 #endif
 
 template <int NB>
@@ -2181,8 +2184,11 @@ __device__ __forceinline__ void cp_async8d(double* dst, const double* src) {
                : "memory");
 }
 
+#ifndef WF_Q64_MINB
+#define WF_Q64_MINB 2
+#endif
 template <int NB>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(128, WF_Q64_MINB)
     quality_tile64_kernel(const QsArgs64 a, double* part_q, double* part_low, double* part_erg,
                           int* undecidable) {
   using L = QsLayout<NB>;
