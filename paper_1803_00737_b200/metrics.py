@@ -462,8 +462,10 @@ def fuse_and_qnr_async(pan, ms, method, *, out=None):
     if not isinstance(method, _fusion.DwtReplace):
         raise TypeError(f"unknown fusion method {method!r}")
     bands = _bands(ms)
+    # (the reference-exact default, WF_EXACT=1 / set_exact_default(True),
+    # fuses with the float64 kernels: fuse() then)
     if method.kind in (WaveletKind.HAAR, WaveletKind.DAUB4) and isinstance(pan, torch.Tensor) \
-            and pan.is_cuda \
+            and not _fusion._exact(None) and pan.is_cuda \
             and pan.dtype == torch.float32 and pan.dim() == 2 and bands \
             and all(isinstance(b, torch.Tensor) and b.dtype == torch.float32 for b in bands):
         h, w = pan.shape
@@ -515,6 +517,7 @@ def fuse_and_qnr(pan, ms, method, *, one_pass: bool | None = None):
     p_shape = tuple(pan.shape) if is_t else np.shape(pan)
     bands = _bands(ms)
     fast = (one_pass is not False and method.kind in (WaveletKind.HAAR, WaveletKind.DAUB4)
+            and not _fusion._exact(None)  # the exact default fuses in float64: fuse() then
             and len(p_shape) == 2
             and bands
             and all(_shape(b) == (p_shape[0] // 2, p_shape[1] // 2) for b in bands)
