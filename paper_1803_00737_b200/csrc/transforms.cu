@@ -539,6 +539,9 @@ static cudaError_t launch_exact_haar(const T* pan, long long pp, const T* const*
 // with every product and sum rounded separately (no FMA), one final cast:
 // bit-identical to the transform path.
 constexpr int kExactRows = 16;
+#ifndef WF_EX_PF  // L1 prefetch distance in row steps: 1 (1.52 ms); 2 -> 1.57, 3 -> 1.66, 4 -> 1.75 (r02_exact_loads_ab.log)
+#define WF_EX_PF 1
+#endif
 
 // Column sharing: a CTA of 128 threads covers 127 output coefficient columns
 // [127k, 127k + 127); thread t computes column j = 127k - 1 + t, so thread 0's
@@ -600,16 +603,16 @@ __global__ void __launch_bounds__(128)
   }
   int buf = 0;
   for (int i = i0; i < i1; ++i, buf ^= 1) {
-    if (i + 1 < i1) {  // next step's PAN and MS lines into L1
+    if (i + WF_EX_PF < i1) {  // the PAN and MS lines of step i + WF_EX_PF into L1
 #pragma unroll
-      for (int r = 4; r < 6; ++r) {
+      for (int r = 2 + 2 * WF_EX_PF; r < 4 + 2 * WF_EX_PF; ++r) {
         const T* row = pan_row(2 * i + r);
         prefetch(row + c0);
         prefetch(row + c3);
       }
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + 1) * mp + j);
+        prefetch(static_cast<const T*>(bands.ms[b]) + (long long)(i + WF_EX_PF) * mp + j);
     }
     // ---- phase 1: column j ----
     rowpass(2 * i + 2, a[2], d[2]);
