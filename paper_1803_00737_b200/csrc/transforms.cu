@@ -553,8 +553,11 @@ constexpr int kExactRows = 16;
 // j-1 again), in the same operations and order.
 constexpr int kExCols = 127;
 
+#ifndef WF_EX_MINB  // CTAs/SM bound: 0 (80 regs, 1.52 ms); 7 -> 72 regs + spills 1.67, 8 -> 1.68
+#define WF_EX_MINB 0
+#endif
 template <typename T, int NB, bool kVec>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, WF_EX_MINB)
     fuse_exact_d4_kernel(const T* __restrict__ pan, long long pp, const ExactBands bands,
                          long long mp, long long op, int H, int W, int rows) {
   // [buffer][quantity][thread]: quantities cvD[0], cvD[1], cvA[b][0], cvA[b][1]
