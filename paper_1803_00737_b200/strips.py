@@ -64,13 +64,17 @@ def exchange_halos(pan: torch.Tensor, ms: list[torch.Tensor], group=None):
         prev = dist.get_global_rank(group, prev)
         nxt = dist.get_global_rank(group, nxt)
     w = pan.shape[1]
-    pan_top = torch.empty((2, w), dtype=pan.dtype, device=pan.device)
-    pan_bot = torch.empty((2, w), dtype=pan.dtype, device=pan.device)
-    ms_top = [torch.empty((1, m.shape[1]), dtype=m.dtype, device=m.device) for m in ms]
+    # gloo moves host tensors only: device strips exchange through host copies
+    # there (plumbing runs); NCCL sends the device rows directly
+    dev = pan.device
+    io = torch.device("cpu") if (pan.is_cuda and dist.get_backend(group) != "nccl") else dev
+    pan_top = torch.empty((2, w), dtype=pan.dtype, device=io)
+    pan_bot = torch.empty((2, w), dtype=pan.dtype, device=io)
+    ms_top = [torch.empty((1, m.shape[1]), dtype=m.dtype, device=io) for m in ms]
     # order-consistent per peer: sends [last2, first2, ms_last...] match the
     # peer's receives [top, bot, ms_top...]
-    last2, first2 = pan[-2:].contiguous(), pan[:2].contiguous()
-    ms_last = [m[-1:].contiguous() for m in ms]
+    last2, first2 = pan[-2:].contiguous().to(io), pan[:2].contiguous().to(io)
+    ms_last = [m[-1:].contiguous().to(io) for m in ms]
     ops = [dist.P2POp(dist.isend, last2, nxt, group),
            dist.P2POp(dist.irecv, pan_top, prev, group),
            dist.P2POp(dist.isend, first2, prev, group),
@@ -80,6 +84,8 @@ def exchange_halos(pan: torch.Tensor, ms: list[torch.Tensor], group=None):
         ops.append(dist.P2POp(dist.irecv, dst, prev, group))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+    if io != dev:
+        return pan_top.to(dev), pan_bot.to(dev), [m.to(dev) for m in ms_top]
     return pan_top, pan_bot, ms_top
 
 
